@@ -1,0 +1,168 @@
+/*
+ * rowblock_b200 — C ABI of the B200-native 1-SA → VBR → SpMM hot path.
+ *
+ * Drop-in boundary for the reference package rowblock v0.1.0
+ * (/root/reference/pkg/src/rowblock).  The reference is pure Python, so its
+ * "FFI" is its Python API; each entry point below replaces one reference
+ * function and the Python host layer (paper_2202_05868_b200/) binds them with
+ * ctypes under the reference's own names and signatures:
+ *
+ *   rb_block_1sa          replaces  block_1sa          blocking.py:283-306
+ *   rb_vbr_plan/emit      replace   vbr_from_grouping  vbr.py:88-125
+ *   rb_spmm_plan_create/  replace   spmm_vbr           multiply.py:72-97
+ *     rb_spmm_execute
+ *
+ * Conventions
+ *   - Plain C: integers, sizes and raw DEVICE pointers (CUDA global memory);
+ *     `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Inputs are never written.  Outputs go to caller-allocated device buffers
+ *     whose sizes are stated per argument (worst case, so no size query is
+ *     needed first) or come from a *_workspace_size query.
+ *   - Calls are stream-ordered.  Calls that must return a data-dependent count
+ *     to the host (n_groups, n_blocks) synchronise `stream` before returning.
+ *   - Return value: RB_OK, or an error code; rb_last_error_string() gives a
+ *     thread-local message.  The Python layer maps RB_EINVAL → ValueError,
+ *     RB_ENOMEM → MemoryError, everything else → RuntimeError (the reference
+ *     raises ValueError for bad shapes/partitions/τ: vbr.py:96-97,
+ *     multiply.py:76-77, blocking.py:80-84).
+ *   - Deterministic: identical inputs give bit-identical outputs; C rows are
+ *     written by exactly one CTA with a fixed accumulation order (no atomics).
+ */
+#ifndef ROWBLOCK_B200_H_
+#define ROWBLOCK_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RB_OK 0
+#define RB_EINVAL 1
+#define RB_ECUDA 2
+#define RB_ENOMEM 3
+#define RB_EUNSUPPORTED 4
+
+/* element types of tiles / B */
+#define RB_F32 0
+#define RB_BF16 1
+#define RB_F16 2
+#define RB_F64 3
+
+/* similarity kinds (MergePolicy.similarity, blocking.py:75) */
+#define RB_JACCARD 0
+#define RB_COSINE 1
+
+const char* rb_last_error_string(void);
+int rb_abi_version(void);
+
+/* ------------------------------------------------------------------ block_1sa
+ * Replaces block_1sa(A, partition, policy, use_compression) (blocking.py:283-306):
+ * quotient bitsets (blocking.py:118-136), exact-pattern compression in first-occurrence
+ * order (295-301), the one-pass greedy scan (209-266) and grouping assembly (269-280).
+ *
+ * Inputs (device): CSR pattern row_ptr[n_rows+1], col_idx[nnz] (int64, columns strictly
+ * increasing per row), column partition boundaries[n_seg+1] (int64, 0 .. n_cols).
+ * Policy: tau in [0,1], similarity RB_JACCARD/RB_COSINE, bounded, pattern_update.
+ * Outputs (device, caller-allocated):
+ *   group_of[n_rows]       RowGrouping.group_of
+ *   row_perm[n_rows]       concatenation of the groups' rows (= VbrMatrix.row_perm)
+ *   group_ptr[n_rows+1]    row extents of each group inside row_perm (first n_groups+1 used)
+ *   seed_size[n_rows]      RowGroup.seed_size (first n_groups used)
+ *   pattern_ptr[n_rows+1], pattern_idx[max(nnz,1)]   RowGroup.pattern (sorted segment ids)
+ *   *n_groups (HOST)       number of groups H
+ */
+int rb_block_1sa_workspace_size(int64_t n_rows, int64_t nnz, int64_t n_seg, int use_compression,
+                                size_t* bytes);
+int rb_block_1sa(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr, const int64_t* col_idx,
+                 const int64_t* boundaries, int64_t n_seg, double tau, int similarity, int bounded,
+                 int pattern_update, int use_compression, void* workspace, size_t workspace_bytes,
+                 int64_t* group_of, int64_t* row_perm, int64_t* group_ptr, int64_t* seed_size,
+                 int64_t* pattern_ptr, int64_t* pattern_idx, int64_t* n_groups, void* stream);
+
+/* ------------------------------------------------------------------ vbr_from_grouping
+ * Replaces vbr_from_grouping(A, grouping, partition) (vbr.py:88-125) in two stream-ordered
+ * phases sharing one workspace (keep it alive from rb_vbr_plan to rb_vbr_emit):
+ *
+ * rb_vbr_plan: stored block columns of each block row recomputed from the data
+ *   (vbr.py:106-112), tile layout.  Inputs: CSR pattern, boundaries, the grouping as
+ *   row_perm[n_rows] / row_partition[H+1] (int64, device).  Outputs (device):
+ *   perm32[n_rows], rpart32[H+1], blk_ptr[H+1] (int32), grp_tile_row[H] (int64: first tile
+ *   row of each block row), bounds32[n_seg+1]; HOST: *n_blocks, *total_tile_rows.
+ *   Tile layout: block t of block row g is an hp(g) x dp row-major tile starting at tile row
+ *   grp_tile_row[g] + t*hp(g), hp(h) = 16 / next pow2 (h <= 128) or roundup(h,128).
+ * rb_vbr_emit: blk_col[n_blocks] (int32, ascending per block row) and the zero-padded
+ *   tiles[total_tile_rows x dp] of tile_dtype (RB_BF16/RB_F16/RB_F32/RB_F64) scattered
+ *   from values[nnz] (float64, device) — vbr.py:113-123.  dp >= max segment width; dp must
+ *   be a multiple of 64 for RB_BF16/RB_F16 (tensor-core path).
+ */
+int rb_vbr_workspace_size(int64_t n_rows, int64_t n_groups, int64_t n_seg, size_t* bytes);
+int rb_vbr_plan(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                const int64_t* boundaries, int64_t n_seg, const int64_t* row_perm, const int64_t* row_partition,
+                int64_t n_groups, void* workspace, size_t workspace_bytes, int32_t* perm32, int32_t* rpart32,
+                int32_t* blk_ptr, int64_t* grp_tile_row, int32_t* bounds32, int64_t* n_blocks,
+                int64_t* total_tile_rows, void* stream);
+int rb_vbr_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                const int64_t* boundaries, int64_t n_seg, int64_t n_groups, void* workspace, size_t workspace_bytes,
+                const int32_t* perm32, const int32_t* rpart32, const int32_t* blk_ptr, const int64_t* grp_tile_row,
+                int32_t* blk_col, void* tiles, int32_t tile_dtype, int32_t dp, int64_t total_tile_rows,
+                void* stream);
+
+/* ------------------------------------------------------------------ spmm_vbr
+ * Replaces spmm_vbr(V, B, threads) (multiply.py:72-97): C = A·B with C rows written at
+ * row_perm positions (un-permute, multiply.py:90); rows of empty block rows are written
+ * as exact zeros (multiply.py:85-86).  C is float32 [n_rows x N] (row stride ldc);
+ * B is [n_cols x N] row-major (row stride ldb, elements), RB_BF16 / RB_F16 (tcgen05
+ * tensor-core path, fp32 accumulate in TMEM) or RB_F32 (fp32 check path, FFMA).
+ * A plan owns its work list (device memory it allocates and frees in _destroy).
+ * Sharding: shard k of n_shards takes a contiguous, work-balanced range of the work list
+ * (whole block-row M-tiles); each C row is produced by exactly one shard.             */
+typedef struct rb_vbr_device {
+  int64_t n_rows;
+  int64_t n_cols;
+  int64_t n_block_rows;          /* H */
+  int64_t n_blocks;              /* nb */
+  int64_t n_seg;
+  int64_t total_tile_rows;
+  int32_t dp;                    /* padded segment width of a tile row */
+  int32_t tile_dtype;            /* RB_BF16 / RB_F16 / RB_F32 */
+  const int32_t* row_partition;  /* [H+1] */
+  const int32_t* row_perm;       /* [n_rows] */
+  const int32_t* blk_ptr;        /* [H+1] */
+  const int32_t* blk_col;        /* [nb] */
+  const int64_t* grp_tile_row;   /* [H] */
+  const int32_t* col_bounds;     /* [n_seg+1] */
+  const void* tiles;             /* [total_tile_rows x dp] */
+} rb_vbr_device;
+
+typedef struct rb_spmm_plan rb_spmm_plan;
+
+typedef struct rb_spmm_info {
+  int64_t n_items_tall;      /* (block row, 128-row M-tile, 256-col N-chunk) work items */
+  int64_t n_items_short;     /* (block row, 256-col N-chunk) swap-AB work items */
+  int64_t n_items_simt;      /* fp32 check-path work items */
+  double executed_flops;     /* 2 * sum over tiles of hp * dp * N_pad (MMA-padded work) */
+  double vbr_flops;          /* 2 * stored_area * N (VBR-padded work) */
+  int64_t row_begin_perm;    /* first permuted row covered by this shard (or -1 if empty) */
+} rb_spmm_info;
+
+int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t b_dtype, int32_t shard,
+                        int32_t n_shards, rb_spmm_plan** plan, void* stream);
+int rb_spmm_plan_info(const rb_spmm_plan* plan, rb_spmm_info* info);
+int rb_spmm_execute(const rb_spmm_plan* plan, const void* B, int64_t ldb, float* C, int64_t ldc, void* stream);
+int rb_spmm_plan_destroy(rb_spmm_plan* plan);
+
+/* ------------------------------------------------------------------ helpers
+ * Element conversion used by the drop-in path (DenseMatrix is float64, matrix.py:107-111):
+ * dst[r, c] (row stride ldd, dtype dst_dtype) = src[r, c] (float64, row stride lds).   */
+int rb_convert_f64(const double* src, int64_t rows, int64_t cols, int64_t lds, void* dst, int32_t dst_dtype,
+                   int64_t ldd, void* stream);
+/* float32 C → float64 (for DenseMatrix returns). */
+int rb_widen_f32(const float* src, int64_t rows, int64_t cols, int64_t lds, double* dst, int64_t ldd,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROWBLOCK_B200_H_ */

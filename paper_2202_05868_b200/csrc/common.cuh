@@ -1,0 +1,42 @@
+// Shared definitions for the rowblock B200 kernels.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/rowblock_b200.h"
+
+namespace rb {
+
+constexpr int kNumSMs = 148;
+
+// Padded block-row height used by the device tile layout:
+//   short block rows (h <= 128) are multiplied in swap-AB orientation, MMA N = hp,
+//   padded to a power of two in [16, 128];
+//   tall block rows (h > 128) are multiplied in M-tiles of 128 rows, hp = roundup(h, 128).
+__host__ __device__ inline int32_t hp_of(int32_t h) {
+  if (h <= 16) return 16;
+  if (h <= 128) {
+    int32_t p = 16;
+    while (p < h) p <<= 1;
+    return p;
+  }
+  return (h + 127) / 128 * 128;
+}
+__host__ __device__ inline bool is_short_row(int32_t h) { return h <= 128; }
+
+// Thread-local error string for rb_last_error_string().
+void set_error(const std::string& s);
+int fail(int code, const std::string& s);
+
+}  // namespace rb
+
+#define RB_CUDA_TRY(expr)                                                                      \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return ::rb::fail(_e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA,                \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                   \
+  } while (0)

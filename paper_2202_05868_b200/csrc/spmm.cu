@@ -1,0 +1,570 @@
+// VBR x dense SpMM on sm_100a: TMA -> SMEM -> tcgen05.mma (bf16/fp16 in, fp32 accumulate in
+// TMEM) -> tcgen05.ld -> un-permuted C rows.  Replaces spmm_vbr (multiply.py:72-97).
+//
+// Two tensor-core kernels share one pipeline skeleton (warp 0 lane 0 = TMA producer,
+// warp 1 lane 0 = MMA issuer, all 4 warps = epilogue):
+//   spmm_tall_kernel   block rows with h > 128: D[128 rows x 256 cols] per work item,
+//                      A = tile rows (K-major, SW128), B = B panel (MN-major, SW128).
+//   spmm_short_kernel  block rows with h <= 128 (swap-AB): D^T[256 cols x hp rows],
+//                      MMA A = B panel (MN-major), MMA B = tile rows (K-major), N = hp.
+// The K loop of a work item runs over the block row's stored blocks (ascending bcol) and
+// the 64-wide K chunks of each block; the B panel of block (g, bcol) is rows
+// col_bounds[bcol] .. +64 of B.  Tile columns beyond the segment width are zero, so B rows
+// of the neighbouring segment (or TMA zero fill past n_cols) contribute exactly 0.
+//
+// spmm_simt_f32_kernel is the fp32 check path (tcgen05 has no fp32-exact MMA).
+#include <algorithm>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <vector>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace rb {
+
+constexpr int KCH = 64;                       // K elements per pipeline stage (one SW128 row)
+constexpr int STAGES = 4;
+constexpr int TALL_BM = 128;
+constexpr int TALL_BN = 256;
+constexpr int SHORT_NS = 256;                 // C columns per short work item (2 x M=128)
+constexpr uint32_t BOX_BYTES = 64 * 64 * 2;   // one [64 k x 64 n] B box
+constexpr uint32_t A_SLOT = 128 * KCH * 2;    // 16 KB
+constexpr uint32_t B_SLOT = KCH * 256 * 2;    // 32 KB
+constexpr uint32_t STAGE_BYTES = A_SLOT + B_SLOT;
+constexpr uint32_t SMEM_TC = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int SIMT_ROWS = 8;
+constexpr int SIMT_COLS = 128;
+
+struct SpmmArgs {
+  const int32_t* row_partition;
+  const int32_t* row_perm;
+  const int32_t* blk_ptr;
+  const int32_t* blk_col;
+  const int64_t* grp_tile_row;
+  const int32_t* col_bounds;
+  const int4* items;
+  int32_t n_items;
+  int32_t dp_chunks;
+  float* C;
+  int64_t ldc;
+  int32_t N;
+  uint32_t ab_fmt;  // 0 = f16, 1 = bf16
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ void store_row_chunk(float* dst, const uint32_t (&r)[32], int ncols, bool vec) {
+  if (vec && ncols >= 32) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                             __uint_as_float(r[j + 3]));
+      *reinterpret_cast<float4*>(dst + j) = v;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < ncols) dst[j] = __uint_as_float(r[j]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// tall block rows: one CTA per (g, m_tile, n0); D = 128 x 256 fp32 in TMEM (256 columns).
+__global__ void __launch_bounds__(128, 1)
+    spmm_tall_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     SpmmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 it = a.items[blockIdx.x];
+  const int g = it.x, m_tile = it.y, n0 = it.z;
+  const int p0 = a.row_partition[g];
+  const int h = a.row_partition[g + 1] - p0;
+  const int hp = hp_of(h);
+  const int b_begin = a.blk_ptr[g];
+  const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
+  const int n_mma = min(TALL_BN, (a.N - n0 + 15) / 16 * 16);
+  const uint32_t idesc = idesc_f16(128, n_mma, a.ab_fmt, /*a_mn=*/0, /*b_mn=*/1);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0 && nk > 0) {
+    // ---------------- TMA producer
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    const int64_t tile_row0 = a.grp_tile_row[g] + (int64_t)m_tile * TALL_BM;
+    const int n_boxes = min(4, (a.N - n0 + 63) / 64);
+    const uint32_t tx = A_SLOT + n_boxes * BOX_BYTES;
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % STAGES;
+      if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) & 1) ^ 1);
+      const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
+      const int bcol = a.blk_col[b_begin + t];
+      uint8_t* sA = smem + s * STAGE_BYTES;
+      uint8_t* sB = sA + A_SLOT;
+      mbar_arrive_expect_tx(&full[s], tx);
+      tma_load_2d(sA, &tmA, &full[s], kc * KCH, (int32_t)(tile_row0 + (int64_t)t * hp));
+      const int krow = a.col_bounds[bcol] + kc * KCH;
+      for (int i = 0; i < n_boxes; ++i) tma_load_2d(sB + i * BOX_BYTES, &tmB, &full[s], n0 + 64 * i, krow);
+    }
+  } else if (warp == 1 && lane == 0 && nk > 0) {
+    // ---------------- MMA issuer (single thread)
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % STAGES;
+      mbar_wait(&full[s], (k / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+      const uint32_t b_base = a_base + A_SLOT;
+#pragma unroll
+      for (int kk = 0; kk < KCH / 16; ++kk) {
+        const uint64_t ad = sdesc_sw128(a_base + kk * 32, 16, 1024);       // K-major, +16 elems = 32 B
+        const uint64_t bd = sdesc_sw128(b_base + kk * 2048, BOX_BYTES, 1024);  // MN-major, +16 rows
+        umma_f16(tmem, ad, bd, idesc, (k | kk) != 0);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tfull);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM lane = tile row, 32 fp32 columns per tcgen05.ld
+  if (nk > 0) {
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+  }
+  const int row_local = m_tile * TALL_BM + warp * 32 + lane;
+  const bool valid = row_local < h;
+  const int64_t crow = valid ? (int64_t)a.row_perm[p0 + row_local] : 0;
+  float* dst = a.C + crow * a.ldc + n0;
+  const bool vec = ((a.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
+  const int ncol = min(TALL_BN, a.N - n0);
+  for (int c = 0; c < ncol; c += 32) {
+    uint32_t r[32];
+    if (nk > 0) {
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+      tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = 0u;
+    }
+    if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------
+// short block rows (swap-AB): one CTA per (g, n0); D_mt^T = B[:, n0+128mt .. +128]^T x tile^T,
+// M = 128 C columns, N = hp tile rows.  TMEM columns [mt*hp, mt*hp + hp).
+__global__ void __launch_bounds__(128, 1)
+    spmm_short_kernel(const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
+                      const __grid_constant__ CUtensorMap tmA64, const __grid_constant__ CUtensorMap tmA128,
+                      const __grid_constant__ CUtensorMap tmB, SpmmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 it = a.items[blockIdx.x];
+  const int g = it.x, n0 = it.z;
+  const int p0 = a.row_partition[g];
+  const int h = a.row_partition[g + 1] - p0;
+  const int hp = hp_of(h);
+  const int b_begin = a.blk_ptr[g];
+  const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
+  const int n_mt = min(2, (a.N - n0 + 127) / 128);
+  const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0 && nk > 0) {
+    const CUtensorMap* tmA = hp == 16 ? &tmA16 : hp == 32 ? &tmA32 : hp == 64 ? &tmA64 : &tmA128;
+    tma_prefetch_desc(tmA);
+    tma_prefetch_desc(&tmB);
+    const int64_t tile_row0 = a.grp_tile_row[g];
+    const int n_boxes = min(4, (a.N - n0 + 63) / 64);
+    const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % STAGES;
+      if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) & 1) ^ 1);
+      const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
+      const int bcol = a.blk_col[b_begin + t];
+      uint8_t* sA = smem + s * STAGE_BYTES;
+      uint8_t* sB = sA + A_SLOT;
+      mbar_arrive_expect_tx(&full[s], tx);
+      tma_load_2d(sA, tmA, &full[s], kc * KCH, (int32_t)(tile_row0 + (int64_t)t * hp));
+      const int krow = a.col_bounds[bcol] + kc * KCH;
+      for (int i = 0; i < n_boxes; ++i) tma_load_2d(sB + i * BOX_BYTES, &tmB, &full[s], n0 + 64 * i, krow);
+    }
+  } else if (warp == 1 && lane == 0 && nk > 0) {
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % STAGES;
+      mbar_wait(&full[s], (k / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t t_base = smem_u32(smem + s * STAGE_BYTES);  // tile rows (K-major)
+      const uint32_t b_base = t_base + A_SLOT;                    // B panel (MN-major)
+      for (int mt = 0; mt < n_mt; ++mt) {
+#pragma unroll
+        for (int kk = 0; kk < KCH / 16; ++kk) {
+          const uint64_t ad = sdesc_sw128(b_base + mt * 2 * BOX_BYTES + kk * 2048, BOX_BYTES, 1024);
+          const uint64_t bd = sdesc_sw128(t_base + kk * 32, 16, 1024);
+          umma_f16(tmem + mt * hp, ad, bd, idesc, (k | kk) != 0);
+        }
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tfull);
+  }
+  __syncwarp();
+
+  if (nk > 0) {
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+  }
+  // epilogue: TMEM lane = C column, TMEM column = block-row row; a warp stores 32 consecutive
+  // columns of one C row per instruction (coalesced 128 B).
+  for (int mt = 0; mt < 2; ++mt) {
+    const int n = n0 + mt * 128 + warp * 32 + lane;
+    const bool nvalid = n < a.N;
+    if (mt >= n_mt) break;
+    for (int j0 = 0; j0 < h; j0 += 16) {
+      uint32_t r[16];
+      if (nk > 0) {
+        tmem_ld_32x32b_x16(tmem + ((uint32_t)(warp * 32) << 16) + mt * hp + j0, r);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = 0u;
+      }
+      if (nvalid) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j0 + j < h) {
+            const int64_t crow = a.row_perm[p0 + j0 + j];
+            a.C[crow * a.ldc + n] = __uint_as_float(r[j]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------
+// fp32 check path: CTA = (g, 8-row chunk r0, 128-col chunk n0); thread = one C column.
+// Per row the accumulation order is blocks ascending, then k ascending (fixed, deterministic).
+__global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, const float* __restrict__ tiles,
+                                                                   int32_t dp, const float* __restrict__ B,
+                                                                   int64_t ldb) {
+  const int4 it = a.items[blockIdx.x];
+  const int g = it.x, r0 = it.y, n0 = it.z;
+  const int p0 = a.row_partition[g];
+  const int h = a.row_partition[g + 1] - p0;
+  const int hp = hp_of(h);
+  const int rows = min(SIMT_ROWS, h - r0);
+  const int n = n0 + threadIdx.x;
+  const bool nv = n < a.N;
+  float acc[SIMT_ROWS];
+#pragma unroll
+  for (int r = 0; r < SIMT_ROWS; ++r) acc[r] = 0.f;
+  const int b0 = a.blk_ptr[g], b1 = a.blk_ptr[g + 1];
+  const int64_t base = a.grp_tile_row[g];
+  for (int b = b0; b < b1; ++b) {
+    const int s = a.blk_col[b];
+    const int k0 = a.col_bounds[s], w = a.col_bounds[s + 1] - k0;
+    const float* t = tiles + (base + (int64_t)(b - b0) * hp + r0) * dp;
+    const float* bp = B + (int64_t)k0 * ldb + n;
+    for (int k = 0; k < w; ++k) {
+      const float bv = nv ? __ldg(bp + (int64_t)k * ldb) : 0.f;
+#pragma unroll
+      for (int r = 0; r < SIMT_ROWS; ++r) acc[r] = __fmaf_rn(__ldg(t + r * dp + k), bv, acc[r]);
+    }
+  }
+  if (nv) {
+    for (int r = 0; r < rows; ++r) a.C[(int64_t)a.row_perm[p0 + r0 + r] * a.ldc + n] = acc[r];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(RB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(RB_EINVAL, "TMA base must be 16-byte aligned");
+  if (row_bytes % 16 != 0) return fail(RB_EINVAL, "TMA row stride must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return RB_OK;
+}
+
+}  // namespace rb
+
+struct rb_spmm_plan {
+  rb_vbr_device v;
+  int64_t N;
+  int32_t b_dtype;
+  int4* d_items = nullptr;  // tall items, then short items, then simt items
+  int64_t n_tall = 0, n_short = 0, n_simt = 0;
+  CUtensorMap tmA16, tmA32, tmA64, tmA128;
+  rb_spmm_info info;
+};
+
+using namespace rb;
+
+extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
+                                   int32_t n_shards, rb_spmm_plan** out, void* stream_) {
+  if (!vbr || !out) return fail(RB_EINVAL, "null argument");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const bool tc = (b_dtype == RB_BF16 || b_dtype == RB_F16);
+  if (!tc && b_dtype != RB_F32) return fail(RB_EUNSUPPORTED, "B dtype must be bf16, f16 or f32");
+  if (tc && vbr->tile_dtype != b_dtype) return fail(RB_EINVAL, "tile dtype must equal B dtype");
+  if (!tc && vbr->tile_dtype != RB_F32) return fail(RB_EINVAL, "fp32 path needs fp32 tiles");
+  if (tc && (vbr->dp <= 0 || vbr->dp % 64 != 0)) return fail(RB_EINVAL, "dp must be a positive multiple of 64");
+  if (N <= 0 || N > (1ll << 30)) return fail(RB_EINVAL, "bad n_dense_cols");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(RB_EINVAL, "bad shard");
+  const int64_t H = vbr->n_block_rows;
+  std::vector<int32_t> rp(H + 1), bp(H + 1);
+  if (H > 0) {
+    RB_CUDA_TRY(cudaMemcpyAsync(rp.data(), vbr->row_partition, sizeof(int32_t) * (H + 1), cudaMemcpyDeviceToHost,
+                                stream));
+    RB_CUDA_TRY(cudaMemcpyAsync(bp.data(), vbr->blk_ptr, sizeof(int32_t) * (H + 1), cudaMemcpyDeviceToHost, stream));
+    RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  // Work units = (block row, row chunk); all column chunks of a unit stay together so each C
+  // row belongs to exactly one shard.  Weight = (blocks + 1) x rows-of-MMA x columns.
+  struct Unit {
+    int32_t g, sub, kind;  // kind 0 tall, 1 short, 2 simt
+    double w;
+  };
+  std::vector<Unit> units;
+  units.reserve(H);
+  const int dpc = tc ? vbr->dp / KCH : 1;
+  for (int64_t g = 0; g < H; ++g) {
+    const int h = rp[g + 1] - rp[g];
+    const int nb = bp[g + 1] - bp[g];
+    if (h <= 0) continue;
+    if (!tc) {
+      for (int r0 = 0; r0 < h; r0 += SIMT_ROWS) units.push_back({(int32_t)g, r0, 2, (nb + 1.0) * SIMT_ROWS});
+    } else if (is_short_row(h)) {
+      units.push_back({(int32_t)g, 0, 1, (nb * dpc + 1.0) * 128.0 * 0.5 * (hp_of(h) / 16 + 1)});
+    } else {
+      for (int m = 0; m < (h + TALL_BM - 1) / TALL_BM; ++m)
+        units.push_back({(int32_t)g, m, 0, (nb * dpc + 1.0) * 256.0});
+    }
+  }
+  double total = 0;
+  for (auto& u : units) total += u.w;
+  const double lo = total * shard / n_shards, hi = total * (shard + 1) / n_shards;
+  std::vector<int4> tall, shrt, simt;
+  double acc = 0;
+  int64_t first_row = -1;
+  double exec_flops = 0, vbr_flops = 0;
+  const int64_t Npad = (N + 15) / 16 * 16;
+  for (auto& u : units) {
+    const double mid = acc + 0.5 * u.w;  // unit goes to the shard owning its midpoint
+    acc += u.w;
+    if (!(mid >= lo && (mid < hi || (shard == n_shards - 1 && mid <= hi)))) continue;
+    const int g = u.g;
+    const int h = rp[g + 1] - rp[g];
+    const int nb = bp[g + 1] - bp[g];
+    if (first_row < 0) first_row = rp[g] + (u.kind == 0 ? u.sub * TALL_BM : u.kind == 2 ? u.sub : 0);
+    if (u.kind == 0) {
+      for (int64_t n0 = 0; n0 < N; n0 += TALL_BN) tall.push_back(make_int4(g, u.sub, (int)n0, nb));
+      exec_flops += 2.0 * nb * TALL_BM * vbr->dp * Npad;
+      vbr_flops += 2.0 * nb * std::min(TALL_BM, h - u.sub * TALL_BM) * (double)vbr->dp * N;
+    } else if (u.kind == 1) {
+      for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS) shrt.push_back(make_int4(g, hp_of(h), (int)n0, nb));
+      exec_flops += 2.0 * nb * hp_of(h) * vbr->dp * ((N + 127) / 128 * 128);
+      vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
+    } else {
+      for (int64_t n0 = 0; n0 < N; n0 += SIMT_COLS) simt.push_back(make_int4(g, u.sub, (int)n0, nb));
+      exec_flops += 2.0 * nb * std::min(SIMT_ROWS, h - u.sub) * (double)vbr->dp * N;
+      vbr_flops += 2.0 * nb * std::min(SIMT_ROWS, h - u.sub) * (double)vbr->dp * N;
+    }
+  }
+  // Longest-first order for the tensor-core kernels (LPT against the tail), stable.
+  auto by_work = [](const int4& x, const int4& y) { return x.w > y.w; };
+  std::stable_sort(tall.begin(), tall.end(), by_work);
+  std::stable_sort(shrt.begin(), shrt.end(), by_work);
+
+  auto* p = new rb_spmm_plan();
+  p->v = *vbr;
+  p->N = N;
+  p->b_dtype = b_dtype;
+  p->n_tall = (int64_t)tall.size();
+  p->n_short = (int64_t)shrt.size();
+  p->n_simt = (int64_t)simt.size();
+  const int64_t n_items = p->n_tall + p->n_short + p->n_simt;
+  if (n_items > 0) {
+    cudaError_t e = cudaMalloc(&p->d_items, sizeof(int4) * n_items);
+    if (e != cudaSuccess) {
+      delete p;
+      return fail(RB_ENOMEM, "cudaMalloc work list");
+    }
+    std::vector<int4> all;
+    all.reserve(n_items);
+    all.insert(all.end(), tall.begin(), tall.end());
+    all.insert(all.end(), shrt.begin(), shrt.end());
+    all.insert(all.end(), simt.begin(), simt.end());
+    e = cudaMemcpyAsync(p->d_items, all.data(), sizeof(int4) * n_items, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      cudaFree(p->d_items);
+      delete p;
+      return fail(RB_ECUDA, cudaGetErrorString(e));
+    }
+  }
+  if (tc && vbr->n_blocks > 0) {
+    if (!vbr->tiles || vbr->total_tile_rows <= 0) {
+      rb_spmm_plan_destroy(p);
+      return fail(RB_EINVAL, "tiles missing");
+    }
+    const CUtensorMapDataType dt = b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    const uint64_t rows = (uint64_t)vbr->total_tile_rows, rb = (uint64_t)vbr->dp * 2;
+    int rc = make_tmap_2d(&p->tmA16, vbr->tiles, dt, vbr->dp, rows, rb, 64, 16);
+    if (!rc) rc = make_tmap_2d(&p->tmA32, vbr->tiles, dt, vbr->dp, rows, rb, 64, 32);
+    if (!rc) rc = make_tmap_2d(&p->tmA64, vbr->tiles, dt, vbr->dp, rows, rb, 64, 64);
+    if (!rc) rc = make_tmap_2d(&p->tmA128, vbr->tiles, dt, vbr->dp, rows, rb, 64, 128);
+    if (rc) {
+      rb_spmm_plan_destroy(p);
+      return rc;
+    }
+  }
+  p->info.n_items_tall = p->n_tall;
+  p->info.n_items_short = p->n_short;
+  p->info.n_items_simt = p->n_simt;
+  p->info.executed_flops = exec_flops;
+  p->info.vbr_flops = vbr_flops;
+  p->info.row_begin_perm = first_row;
+  *out = p;
+  return RB_OK;
+}
+
+extern "C" int rb_spmm_plan_info(const rb_spmm_plan* p, rb_spmm_info* info) {
+  if (!p || !info) return fail(RB_EINVAL, "null argument");
+  *info = p->info;
+  return RB_OK;
+}
+
+extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
+  if (!p) return RB_OK;
+  if (p->d_items) cudaFree(p->d_items);
+  delete p;
+  return RB_OK;
+}
+
+extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
+                               void* stream_) {
+  if (!p) return fail(RB_EINVAL, "null plan");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (ldc < p->N || ldb < p->N) return fail(RB_EINVAL, "leading dimension smaller than N");
+  if (!C && p->v.n_rows > 0) return fail(RB_EINVAL, "null C");
+  SpmmArgs a;
+  a.row_partition = p->v.row_partition;
+  a.row_perm = p->v.row_perm;
+  a.blk_ptr = p->v.blk_ptr;
+  a.blk_col = p->v.blk_col;
+  a.grp_tile_row = p->v.grp_tile_row;
+  a.col_bounds = p->v.col_bounds;
+  a.dp_chunks = p->v.dp / KCH;
+  a.C = C;
+  a.ldc = ldc;
+  a.N = (int32_t)p->N;
+  a.ab_fmt = p->b_dtype == RB_BF16 ? 1u : 0u;
+  if (p->b_dtype == RB_F32) {
+    if (p->n_simt > 0) {
+      a.items = p->d_items;
+      a.n_items = (int32_t)p->n_simt;
+      a.dp_chunks = 1;
+      spmm_simt_f32_kernel<<<(unsigned)p->n_simt, SIMT_COLS, 0, stream>>>(
+          a, static_cast<const float*>(p->v.tiles), p->v.dp, static_cast<const float*>(B), ldb);
+      RB_CUDA_TRY(cudaGetLastError());
+    }
+    return RB_OK;
+  }
+  static bool attr_done = false;
+  if (!attr_done) {
+    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
+    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
+    attr_done = true;
+  }
+  CUtensorMap tmB;
+  memset(&tmB, 0, sizeof(tmB));
+  if (p->v.n_blocks > 0) {
+    const CUtensorMapDataType dt =
+        p->b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    int rc = make_tmap_2d(&tmB, B, dt, (uint64_t)p->N, (uint64_t)p->v.n_cols, (uint64_t)ldb * 2, 64, 64);
+    if (rc) return rc;
+  }
+  if (p->n_tall > 0) {
+    a.items = p->d_items;
+    a.n_items = (int32_t)p->n_tall;
+    spmm_tall_kernel<<<(unsigned)p->n_tall, 128, SMEM_TC, stream>>>(p->tmA128, tmB, a);
+    RB_CUDA_TRY(cudaGetLastError());
+  }
+  if (p->n_short > 0) {
+    a.items = p->d_items + p->n_tall;
+    a.n_items = (int32_t)p->n_short;
+    spmm_short_kernel<<<(unsigned)p->n_short, 128, SMEM_TC, stream>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
+                                                                        tmB, a);
+    RB_CUDA_TRY(cudaGetLastError());
+  }
+  return RB_OK;
+}

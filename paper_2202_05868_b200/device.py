@@ -1,0 +1,296 @@
+"""Device-resident forms of the hot-path objects and the torch-native API.
+
+    DeviceCsr       CSR pattern + values in HBM (int64 / float64, as CsrMatrix)
+    DeviceGrouping  output of block_1sa on the device (RowGrouping arrays)
+    DeviceVbr       VBR structure + padded tiles in HBM (see DESIGN.md §3 for the layout)
+
+``block_1sa_device`` → ``DeviceVbr.build`` → ``DeviceVbr.spmm`` is the hot path
+with every buffer resident in HBM; the reference-facing functions in
+``blocking.py`` / ``vbr.py`` / ``multiply.py`` wrap these with host copies.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import warnings
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .types import ColumnPartition, MergePolicy, RowGroup, RowGrouping, VbrBlock
+
+
+def host_tensor(a: np.ndarray) -> torch.Tensor:
+    """Zero-copy CPU tensor over a (possibly read-only, frozen) numpy array; it is only ever read."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(np.ascontiguousarray(a))
+
+
+def _i64(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.int64).contiguous()
+    return host_tensor(np.asarray(x, dtype=np.int64)).to(device)
+
+
+def hp_of(h: int) -> int:
+    """Padded tile height (mirrors csrc/common.cuh hp_of)."""
+    if h <= 16:
+        return 16
+    if h <= 128:
+        p = 16
+        while p < h:
+            p <<= 1
+        return p
+    return (h + 127) // 128 * 128
+
+
+class DeviceCsr:
+    """CSR in device memory; ``row_ptr``/``col_idx`` int64, ``values`` float64."""
+
+    def __init__(self, n_rows: int, n_cols: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
+                 values: torch.Tensor | None):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_ptr, self.col_idx, self.values = row_ptr, col_idx, values
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @classmethod
+    def from_host(cls, A, device=None) -> "DeviceCsr":
+        dev = device or L.require_cuda()
+        vals = host_tensor(np.asarray(A.values, dtype=np.float64)).to(dev)
+        return cls(A.n_rows, A.n_cols, _i64(A.row_ptr, dev), _i64(A.col_idx, dev), vals)
+
+
+def _boundaries(partition, n_cols: int, device) -> tuple[torch.Tensor, np.ndarray]:
+    b = np.asarray(partition.boundaries if hasattr(partition, "boundaries") else partition, dtype=np.int64)
+    if int(getattr(partition, "n_cols", b[-1] if b.size else 0)) != n_cols:
+        raise ValueError("grouping/partition inconsistent with matrix dimensions")
+    return _i64(b, device), b
+
+
+class DeviceGrouping:
+    """block_1sa result in device memory (int64 arrays, RowGrouping semantics)."""
+
+    def __init__(self, n_rows, n_groups, group_of, row_perm, group_ptr, seed_size, pattern_ptr, pattern_idx):
+        self.n_rows, self.n_groups = int(n_rows), int(n_groups)
+        self.group_of, self.row_perm, self.group_ptr = group_of, row_perm, group_ptr
+        self.seed_size, self.pattern_ptr, self.pattern_idx = seed_size, pattern_ptr, pattern_idx
+
+    def to_host(self) -> RowGrouping:
+        """Materialise the reference's RowGrouping (tuple of RowGroup, blocking.py:269-280)."""
+        H = self.n_groups
+        go = self.group_of.cpu().numpy()
+        rp = self.row_perm.cpu().numpy()
+        gp = self.group_ptr[: H + 1].cpu().numpy()
+        ss = self.seed_size[:H].cpu().numpy()
+        pp = self.pattern_ptr[: H + 1].cpu().numpy()
+        pi = self.pattern_idx[: int(pp[-1]) if H else 0].cpu().numpy()
+        groups = [RowGroup(rp[gp[g]:gp[g + 1]], pi[pp[g]:pp[g + 1]], int(ss[g])) for g in range(H)]
+        return RowGrouping(go, groups, device=self)
+
+
+def block_1sa_device(A: DeviceCsr, partition, policy: MergePolicy, use_compression: bool = True,
+                     stream=None) -> DeviceGrouping:
+    """Device block_1sa (blocking.py:283-306) through rb_block_1sa."""
+    if policy.similarity not in ("jaccard", "cosine"):
+        raise ValueError(f"unknown similarity {policy.similarity!r}")
+    if not 0.0 <= float(policy.tau) <= 1.0:
+        raise ValueError("tau must be in [0, 1]")
+    dev = A.row_ptr.device
+    bnd, bh = _boundaries(partition, A.n_cols, dev)
+    n_seg = len(bh) - 1
+    n = A.n_rows
+    lib = L.lib()
+    ws_bytes = ctypes.c_size_t(0)
+    L.check(lib.rb_block_1sa_workspace_size(n, A.nnz, n_seg, int(bool(use_compression)), ctypes.byref(ws_bytes)))
+    ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=dev)
+    group_of = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    row_perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    group_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    seed_size = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    pattern_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    pattern_idx = torch.empty(max(A.nnz, 1), dtype=torch.int64, device=dev)
+    H = ctypes.c_int64(0)
+    L.check(lib.rb_block_1sa(n, A.n_cols, A.nnz, L.ptr(A.row_ptr), L.ptr(A.col_idx), L.ptr(bnd), n_seg,
+                             float(policy.tau), L.RB_COSINE if policy.similarity == "cosine" else L.RB_JACCARD,
+                             int(bool(policy.bounded)), int(bool(policy.pattern_update)), int(bool(use_compression)),
+                             L.ptr(ws), ws_bytes.value, L.ptr(group_of), L.ptr(row_perm), L.ptr(group_ptr),
+                             L.ptr(seed_size), L.ptr(pattern_ptr), L.ptr(pattern_idx), ctypes.byref(H),
+                             L.stream_handle(stream)))
+    return DeviceGrouping(n, H.value, group_of[:n], row_perm[:n], group_ptr, seed_size, pattern_ptr, pattern_idx)
+
+
+class DeviceVbr:
+    """VBR matrix resident in HBM.
+
+    Structure (int32): row_partition[H+1], row_perm[n], blk_ptr[H+1], blk_col[nb],
+    grp_tile_row[H] (int64), col_bounds[n_seg+1].  Tiles: block t of block row g is an
+    hp(h_g) x dp row-major tile at tile row grp_tile_row[g] + t*hp(h_g); one tile array per dtype.
+    """
+
+    def __init__(self):
+        self._plans: dict = {}
+        self.tiles: dict = {}
+        self._finalizer = None
+
+    # ---------------------------------------------------------------- build (rb_vbr_plan / emit)
+    @classmethod
+    def build(cls, A: DeviceCsr, partition, row_perm, row_partition, dtypes=("bf16",), stream=None) -> "DeviceVbr":
+        dev = A.row_ptr.device
+        self = cls()
+        self.csr = A
+        self.n_rows, self.n_cols = A.n_rows, A.n_cols
+        self.boundaries, bh = _boundaries(partition, A.n_cols, dev)
+        self.boundaries_host = bh
+        self.n_seg = len(bh) - 1
+        self.max_width = int(np.diff(bh).max()) if self.n_seg else 0
+        self.row_perm64 = _i64(row_perm, dev)
+        self.row_partition64 = _i64(row_partition, dev)
+        if self.row_perm64.numel() != A.n_rows:
+            raise ValueError("grouping/partition inconsistent with matrix dimensions")
+        H = self.row_partition64.numel() - 1
+        self.n_block_rows = H
+        lib = L.lib()
+        wsb = ctypes.c_size_t(0)
+        L.check(lib.rb_vbr_workspace_size(A.n_rows, H, self.n_seg, ctypes.byref(wsb)))
+        self._ws = torch.empty(max(1, wsb.value), dtype=torch.uint8, device=dev)
+        n = A.n_rows
+        self.row_perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.row_partition = torch.empty(H + 1, dtype=torch.int32, device=dev)
+        self.blk_ptr = torch.empty(H + 1, dtype=torch.int32, device=dev)
+        self.grp_tile_row = torch.empty(max(H, 1), dtype=torch.int64, device=dev)
+        self.col_bounds = torch.empty(self.n_seg + 1, dtype=torch.int32, device=dev)
+        nb, rows = ctypes.c_int64(0), ctypes.c_int64(0)
+        L.check(lib.rb_vbr_plan(A.n_rows, A.n_cols, L.ptr(A.row_ptr), L.ptr(A.col_idx), L.ptr(self.boundaries),
+                                self.n_seg, L.ptr(self.row_perm64), L.ptr(self.row_partition64), H, L.ptr(self._ws),
+                                wsb.value, L.ptr(self.row_perm), L.ptr(self.row_partition), L.ptr(self.blk_ptr),
+                                L.ptr(self.grp_tile_row), L.ptr(self.col_bounds), ctypes.byref(nb),
+                                ctypes.byref(rows), L.stream_handle(stream)))
+        self.n_blocks, self.total_tile_rows = nb.value, rows.value
+        self.blk_col = torch.empty(max(self.n_blocks, 1), dtype=torch.int32, device=dev)
+        self._ws_bytes = wsb.value
+        self._blkcol_done = False
+        for d in dtypes:
+            self.tiles_for(d, stream=stream)
+        if not self._blkcol_done:
+            self._emit(None, L.RB_F32, self.dp_for(L.RB_F32), stream)
+        return self
+
+    def dp_for(self, tile_dtype: int) -> int:
+        w = max(self.max_width, 1)
+        return (w + 63) // 64 * 64 if tile_dtype in (L.RB_BF16, L.RB_F16) else (w + 3) // 4 * 4
+
+    def _emit(self, tiles, tile_dtype, dp, stream):
+        L.check(L.lib().rb_vbr_emit(self.n_rows, L.ptr(self.csr.row_ptr), L.ptr(self.csr.col_idx),
+                                    L.ptr(self.csr.values), L.ptr(self.boundaries), self.n_seg, self.n_block_rows,
+                                    L.ptr(self._ws), self._ws_bytes, L.ptr(self.row_perm), L.ptr(self.row_partition),
+                                    L.ptr(self.blk_ptr), L.ptr(self.grp_tile_row), L.ptr(self.blk_col),
+                                    L.ptr(tiles), tile_dtype, dp, self.total_tile_rows if tiles is not None else 0,
+                                    L.stream_handle(stream)))
+        self._blkcol_done = True
+
+    def tiles_for(self, precision, stream=None) -> tuple[torch.Tensor, int]:
+        """(tiles, dp) of the given precision ("bf16"/"fp16"/"fp32" or an RB_* code), built on demand."""
+        td = L.PRECISION[precision] if isinstance(precision, str) else int(precision)
+        if td not in self.tiles:
+            dp = self.dp_for(td)
+            t = torch.empty((max(self.total_tile_rows, 1), dp), dtype=L.TORCH_DTYPE[td], device=self.blk_ptr.device)
+            self._emit(t, td, dp, stream)
+            self.tiles[td] = (t, dp)
+        return self.tiles[td]
+
+    # ---------------------------------------------------------------- SpMM (rb_spmm_*)
+    def _struct(self, td: int) -> L.VbrDevice:
+        t, dp = self.tiles_for(td)
+        return L.VbrDevice(self.n_rows, self.n_cols, self.n_block_rows, self.n_blocks, self.n_seg,
+                           self.total_tile_rows, dp, td, self.row_partition.data_ptr(), self.row_perm.data_ptr(),
+                           self.blk_ptr.data_ptr(), self.blk_col.data_ptr(), self.grp_tile_row.data_ptr(),
+                           self.col_bounds.data_ptr(), t.data_ptr())
+
+    def plan(self, N: int, precision="bf16", shard: int = 0, n_shards: int = 1, stream=None):
+        td = L.PRECISION[precision] if isinstance(precision, str) else int(precision)
+        key = (int(N), td, int(shard), int(n_shards))
+        if key not in self._plans:
+            s = self._struct(td)
+            h = ctypes.c_void_p(0)
+            L.check(L.lib().rb_spmm_plan_create(ctypes.byref(s), int(N), td, int(shard), int(n_shards),
+                                                ctypes.byref(h), L.stream_handle(stream)))
+            self._plans[key] = h
+            if self._finalizer is None:
+                self._finalizer = weakref.finalize(self, DeviceVbr._destroy_plans, self._plans)
+        return self._plans[key]
+
+    @staticmethod
+    def _destroy_plans(plans):
+        try:
+            lib = L.lib()
+        except Exception:  # interpreter shutdown
+            return
+        for h in plans.values():
+            lib.rb_spmm_plan_destroy(h)
+        plans.clear()
+
+    def plan_info(self, N: int, precision="bf16", shard: int = 0, n_shards: int = 1) -> dict:
+        info = L.SpmmInfo()
+        L.check(L.lib().rb_spmm_plan_info(self.plan(N, precision, shard, n_shards), ctypes.byref(info)))
+        return {f: getattr(info, f) for f, _ in L.SpmmInfo._fields_}
+
+    def spmm(self, B: torch.Tensor, out: torch.Tensor | None = None, precision: str | None = None,
+             shard: int = 0, n_shards: int = 1, stream=None) -> torch.Tensor:
+        """C[n_rows, N] (float32) = A @ B on the device.  B: [n_cols, N] bf16/fp16/fp32 (row stride
+        a multiple of 8 elements for 16-bit types).  ``out`` rows not owned by ``shard`` are untouched."""
+        if B.dim() != 2 or B.shape[0] != self.n_cols:
+            raise ValueError(f"dimension mismatch: {self.n_cols} vs {B.shape[0] if B.dim() == 2 else B.shape}")
+        prec = precision or {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}[B.dtype]
+        if L.TORCH_DTYPE[L.PRECISION[prec]] != B.dtype:
+            raise ValueError(f"B dtype {B.dtype} does not match precision {prec}")
+        N = B.shape[1]
+        if B.stride(1) != 1:
+            raise ValueError("B must be row-major (stride(1) == 1)")
+        if out is None:
+            out = torch.empty((self.n_rows, N), dtype=torch.float32, device=B.device)
+        if out.dtype != torch.float32 or out.shape != (self.n_rows, N) or out.stride(1) != 1:
+            raise ValueError("out must be float32 [n_rows, N], row-major")
+        if N == 0 or self.n_rows == 0:
+            return out
+        h = self.plan(N, prec, shard, n_shards, stream)
+        L.check(L.lib().rb_spmm_execute(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0),
+                                        L.stream_handle(stream)))
+        return out
+
+    # ---------------------------------------------------------------- reference-format views
+    def host_structure(self):
+        rp = self.row_partition.cpu().numpy().astype(np.int64)
+        bp = self.blk_ptr.cpu().numpy().astype(np.int64)
+        bc = self.blk_col[: self.n_blocks].cpu().numpy().astype(np.int64)
+        return rp, bp, bc
+
+    def stored_area(self) -> int:
+        rp, bp, bc = self.host_structure()
+        widths = np.diff(self.boundaries_host)
+        heights = np.diff(rp)
+        blk_h = np.repeat(heights, np.diff(bp))
+        return int(np.sum(blk_h * widths[bc])) if len(bc) else 0
+
+    def host_block_rows(self) -> tuple:
+        """float64 payloads (vbr.py:113-123) via a float64 tile emission on the device."""
+        t, dp = self.tiles_for(L.RB_F64)
+        tiles = t.cpu().numpy()
+        del self.tiles[L.RB_F64]
+        rp, bp, bc = self.host_structure()
+        tr = self.grp_tile_row[: self.n_block_rows].cpu().numpy()
+        widths = np.diff(self.boundaries_host)
+        out = []
+        for g in range(self.n_block_rows):
+            h = int(rp[g + 1] - rp[g])
+            hp = hp_of(h)
+            base = int(tr[g])
+            out.append(tuple(VbrBlock(int(bc[k]), tiles[base + (k - bp[g]) * hp: base + (k - bp[g]) * hp + h,
+                                                          : int(widths[bc[k]])])
+                             for k in range(int(bp[g]), int(bp[g + 1]))))
+        return tuple(out)

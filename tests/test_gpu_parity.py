@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against reference-generated golden vectors and the oracle.
+
+Structure (1-SA grouping, VBR block structure, payload reconstruction) must be
+bit-exact.  C tolerances (fp32 accumulation, stated here):
+  * fp32 check path vs the reference's float64 C:            |err| <= 1e-5 * (|A|·|B|)
+  * bf16 / fp16 tensor-core path vs the float64 product of the SAME bf16/fp16-rounded
+    inputs (only fp32 accumulation differs):                   |err| <= 1e-4 * (|A|·|B|)
+  * bf16 tensor-core path vs the reference on the raw float64 inputs: rel <= 1e-2
+    (north_star tolerance) measured as |err| <= 1e-2 * (|A|·|B|)
+Rows of A without nonzeros must come out exactly 0.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2202_05868_b200 as rb
+from conftest import MEDIUM, golden_b, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def csr_of(case):
+    return rb.CsrMatrix(int(case["n_rows"]), int(case["n_cols"]), case["row_ptr"], case["col_idx"], case["values"])
+
+
+def part_of(case):
+    return rb.ColumnPartition(int(case["n_cols"]), case["boundaries"])
+
+
+def policy_of(case):
+    return rb.MergePolicy(similarity="cosine" if int(case["cosine"]) else "jaccard", tau=float(case["tau"]),
+                          bounded=bool(case["bounded"]), pattern_update=bool(case["pattern_update"]))
+
+
+def check_grouping(g, case, name=""):
+    assert np.array_equal(g.group_of, case["group_of"]), name
+    rows = np.concatenate([gr.rows for gr in g.groups]) if g.n_groups else np.zeros(0, np.int64)
+    assert np.array_equal(rows, case["row_perm"]), name
+    assert np.array_equal(np.concatenate([[0], np.cumsum(g.heights())]), case["row_partition"]), name
+    assert np.array_equal(np.array([gr.seed_size for gr in g.groups], np.int64), case["seed_size"]), name
+    pats = np.concatenate([gr.pattern for gr in g.groups]) if g.n_groups else np.zeros(0, np.int64)
+    assert np.array_equal(pats, case["pattern_idx"]), name
+    assert np.array_equal(np.concatenate([[0], np.cumsum([len(gr.pattern) for gr in g.groups])]),
+                          case["pattern_ptr"]), name
+
+
+def check_vbr_structure(V, case, name=""):
+    assert np.array_equal(V.row_perm, case["row_perm"]), name
+    assert np.array_equal(V.row_partition, case["row_partition"]), name
+    rp, bp, bc = V.device.host_structure()
+    assert np.array_equal(bp, case["blk_ptr"]), name
+    assert np.array_equal(bc, case["blk_col"]), name
+    assert V.stored_area == int(case["stored_area"]), name
+
+
+def vbr_to_dense(V):
+    out = np.zeros((V.n_rows, V.n_cols))
+    b = V.col_partition.boundaries
+    for g in range(V.n_block_rows):
+        rows = V.row_perm[V.row_partition[g]:V.row_partition[g + 1]]
+        for blk in V.block_rows[g]:
+            out[rows, b[blk.bcol]:b[blk.bcol + 1]] = blk.data
+    return out
+
+
+def rounded(x, dt):
+    """Correctly rounded (RNE) float64 -> dt -> float64, as the device's __double2bfloat16 /
+    __double2half do (torch's .to(bfloat16) rounds twice, via float32)."""
+    x = np.asarray(x, np.float64)
+    if dt == torch.float16:
+        return x.astype(np.float16).astype(np.float64)
+    b = np.ascontiguousarray(x).view(np.uint64)
+    lsb = (b >> np.uint64(45)) & np.uint64(1)
+    r = (b + np.uint64((1 << 44) - 1) + lsb) & ~np.uint64((1 << 45) - 1)
+    return r.view(np.float64)
+
+
+def dense_of(case, dt=None):
+    A = np.zeros((int(case["n_rows"]), int(case["n_cols"])))
+    rows = np.repeat(np.arange(int(case["n_rows"])), np.diff(case["row_ptr"]))
+    vals = case["values"] if dt is None else rounded(case["values"], dt)
+    A[rows, case["col_idx"]] = vals
+    return A
+
+
+def assert_close(C, ref, bound, rtol, name=""):
+    err = np.abs(C - ref)
+    assert np.all(err <= rtol * bound + 1e-30), f"{name}: max scaled err {np.max(err / (bound + 1e-30)):.3e}"
+
+
+# ------------------------------------------------------------------ 1-SA + VBR structure
+
+
+def test_block_1sa_bit_exact_golden_small(golden_small):
+    for name, case in golden_small.items():
+        g = rb.block_1sa(csr_of(case), part_of(case), policy_of(case), bool(case["use_compression"]))
+        check_grouping(g, case, name)
+
+
+def test_vbr_structure_and_reconstruction_golden_small(golden_small):
+    for name, case in golden_small.items():
+        A = csr_of(case)
+        q = part_of(case)
+        g = rb.block_1sa(A, q, policy_of(case), bool(case["use_compression"]))
+        V = rb.vbr_from_grouping(A, g, q)
+        check_vbr_structure(V, case, name)
+        assert np.array_equal(vbr_to_dense(V), A.to_dense()), name  # bit-exact (test_vbr.py:73-88)
+
+
+@pytest.mark.parametrize("name", MEDIUM)
+def test_block_1sa_and_vbr_medium(name):
+    case = load_golden(name)
+    A, q = csr_of(case), part_of(case)
+    g = rb.block_1sa(A, q, policy_of(case), bool(case["use_compression"]))
+    check_grouping(g, case, name)
+    V = rb.vbr_from_grouping(A, g, q)
+    check_vbr_structure(V, case, name)
+
+
+# ------------------------------------------------------------------ SpMM
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16", "fp16"])
+def test_spmm_golden_small(golden_small, precision):
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": None}[precision]
+    n_checked = 0
+    for name, case in golden_small.items():
+        B = golden_b(case)
+        if B is None or "C" not in case:
+            continue
+        A, q = csr_of(case), part_of(case)
+        V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), bool(case["use_compression"])), q)
+        C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision=precision).data
+        Ad = dense_of(case)
+        bound = np.abs(Ad) @ np.abs(B)
+        if precision == "fp32":
+            assert_close(C, case["C"], bound, 1e-5, name)
+        else:
+            ref_r = dense_of(case, tdt) @ rounded(B, tdt)
+            assert_close(C, ref_r, np.abs(dense_of(case, tdt)) @ np.abs(rounded(B, tdt)), 1e-4, name)
+            if precision == "bf16":
+                assert_close(C, case["C"], bound, 1e-2, name)
+        empty = np.diff(case["row_ptr"]) == 0
+        assert np.all(C[empty] == 0.0), name
+        n_checked += 1
+    assert n_checked > 100
+
+
+@pytest.mark.parametrize("name", ["cfg1_full", "cfg4_s8", "cfg5_s32"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_spmm_medium_checksums(name, precision):
+    case = load_golden(name)
+    B = golden_b(case)
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision=precision).data
+    r = np.random.default_rng(7).standard_normal(B.shape[1])
+    tol = 1e-5 if precision == "fp32" else 1e-2
+    scale = (np.abs(A.to_dense()) @ np.abs(B)) @ np.abs(r)
+    assert np.all(np.abs(C @ r - case["C_dot_r"]) <= tol * scale + 1e-12)
+    assert np.all(np.abs(C.sum(axis=1) - case["C_rowsum"]) <= tol * (np.abs(A.to_dense()) @ np.abs(B)).sum(1) + 1e-12)
+
+
+def test_spmm_tall_and_short_shapes_bf16():
+    """Exercise both tensor-core kernels: tall block rows (h > 128, several M-tiles, ragged last
+    tile), short block rows of every padded height (16/32/64/128), N not a multiple of 64,
+    Δ > 64 (two K chunks per block), ragged last segment."""
+    rng = np.random.default_rng(5)
+    heights = [1, 3, 16, 17, 40, 64, 100, 128, 129, 300, 513]
+    n_cols, delta, N = 1000, 96, 200
+    rows, cols = [], []
+    r0 = 0
+    for h in heights:
+        segs = rng.choice((n_cols + delta - 1) // delta, size=int(rng.integers(1, 6)), replace=False)
+        for s in segs:
+            lo, hi = s * delta, min(n_cols, (s + 1) * delta)
+            for r in range(r0, r0 + h):
+                c = rng.choice(np.arange(lo, hi), size=max(1, (hi - lo) // 5), replace=False)
+                rows.append(np.full(len(c), r))
+                cols.append(c)
+        r0 += h
+    n_rows = r0
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    vals = rounded(rng.uniform(-1, 1, len(rows)), torch.bfloat16)
+    keep = vals != 0
+    from paper_2202_05868_b200.types import csr_from_coo
+    A = csr_from_coo(n_rows, n_cols, rows[keep], cols[keep], vals[keep], sum_duplicates=True)
+    perm = rng.permutation(n_rows)  # groups by construction, rows scrambled inside the grouping
+    q = rb.ColumnPartition.uniform(n_cols, delta)
+    groups, start = [], 0
+    from paper_2202_05868_b200.types import RowGroup, RowGrouping
+    go = np.zeros(n_rows, np.int64)
+    for gi, h in enumerate(heights):
+        members = np.arange(start, start + h)
+        go[members] = gi
+        groups.append(RowGroup(members, np.zeros(0), 0))
+        start += h
+    G = RowGrouping(go, groups)
+    V = rb.vbr_from_grouping(A, G, q)
+    B = rounded(rng.uniform(-1, 1, (n_cols, N)), torch.bfloat16)
+    C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision="bf16").data
+    ref = A.to_dense() @ B
+    assert_close(C, ref, np.abs(A.to_dense()) @ np.abs(B), 1e-4, "shapes")
+    del perm
+
+
+def test_spmm_device_api_and_determinism():
+    rng = np.random.default_rng(9)
+    case = load_golden("cfg5_s32")
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    B = torch.rand((A.n_cols, 256), device="cuda").to(torch.bfloat16)
+    C1 = rb.spmm_vbr_device(V, B)
+    C2 = rb.spmm_vbr_device(V, B)
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)  # bit-identical run to run
+    ref = torch.from_numpy(A.to_dense()).cuda().to(torch.bfloat16).double() @ B.double()
+    err = (C1.double() - ref).abs().max().item()
+    assert err <= 1e-4 * ref.abs().max().item()
+    del rng
+
+
+def test_errors_map_to_reference_exceptions():
+    A = rb.csr_from_triplets(4, 6, [(0, 0, 1.0), (0, 1, 1.0), (1, 3, 1.0), (2, 2, 1.0), (3, 4, 1.0), (3, 5, 1.0)])
+    q = rb.ColumnPartition.uniform(6, 3)
+    g = rb.block_1sa(A, q, rb.MergePolicy(tau=0.5))
+    with pytest.raises(ValueError):
+        rb.vbr_from_grouping(A, g, rb.ColumnPartition.uniform(5, 3))
+    V = rb.vbr_from_grouping(A, g, q)
+    with pytest.raises(ValueError):
+        rb.spmm_vbr(V, rb.DenseMatrix.zeros(5, 2))
+    with pytest.raises(ValueError):
+        rb.MergePolicy(tau=1.5)
