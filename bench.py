@@ -1,0 +1,436 @@
+"""Benchmark: VBR SpMM effective GFLOP/s (2·nnz·N/s) on B200 vs the CPU reference path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One "step" = one pass of the hot path's SpMM over the whole synthetic workload
+(C = A·B with A resident as VBR tiles in HBM, B resident, C written in HBM).
+Setup (synthesis, 1-SA, VBR build) runs before the timed region and is reported
+under "stages".  For N>1 (torchrun) every rank owns a work-balanced shard of the
+work list (whole block-row M-tiles: disjoint C rows, no data-path collective);
+timing is the max over ranks.  See DESIGN.md §5 for the measurement protocol.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VBR SpMM effective GFLOP/s (2·nnz·N/s) + tensor-pipe util, 1–8 B200 vs CPU ref"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="2")
+    p.add_argument("--scale", type=int, default=1)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------------------- helpers
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+def profile_traffic(config: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get(config)
+    return None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML every 5 ms while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_sample(A_host, bounds, row_perm, row_partition, group_width, N, target_flops):
+    """A bounded prefix of the permuted rows (whole block rows, the last one truncated) as a
+    standalone VBR problem for the oracle port of spmm_vbr (multiply.py:72-97).
+    group_width[g] = total stored-segment width of block row g (VBR-padded flops/row = 2*width*N)."""
+    import oracle
+
+    rp_ptr, cols, vals = A_host
+    rp = np.asarray(row_partition, np.int64)
+    perm = np.asarray(row_perm, np.int64)
+    flops, P, cuts = 0.0, 0, [0]
+    for g in range(len(rp) - 1):
+        h = int(rp[g + 1] - rp[g])
+        per_row = 2.0 * max(1, int(group_width[g])) * N
+        take = h
+        if flops + per_row * take > target_flops:
+            take = max(1, int((target_flops - flops) / per_row))
+        P += take
+        cuts.append(P)
+        flops += per_row * take
+        if take < h or flops >= target_flops:
+            break
+    sel = perm[:P]
+    counts = rp_ptr[sel + 1] - rp_ptr[sel]
+    sp = np.zeros(P + 1, np.int64)
+    np.cumsum(counts, out=sp[1:])
+    idx = np.repeat(rp_ptr[sel] - sp[:-1], counts) + np.arange(int(sp[-1]))
+    s_cols, s_vals = cols[idx], vals[idx]
+    s_perm = np.arange(P)
+    s_rp = np.asarray(cuts, np.int64)
+    bp, bc = oracle.vbr_blocks(sp, s_cols, bounds, s_perm, s_rp)
+    pay = oracle.vbr_payloads(sp, s_cols, s_vals, bounds, s_perm, s_rp, bp, bc)
+    return dict(payloads=pay, row_perm=s_perm, row_partition=s_rp, nnz=int(len(s_cols)), rows=P,
+                block_rows=len(cuts) - 1)
+
+
+def group_widths(bounds, row_partition, blk_ptr, blk_col):
+    w = np.diff(np.asarray(bounds, np.int64))
+    bp = np.asarray(blk_ptr, np.int64)
+    per_blk = w[np.asarray(blk_col, np.int64)] if len(blk_col) else np.zeros(0, np.int64)
+    cs = np.concatenate([[0], np.cumsum(per_blk)])
+    return cs[bp[1:]] - cs[bp[:-1]]
+
+
+def time_cpu(sample, bounds, B64, threads, repeats=1):
+    import oracle
+
+    best = math.inf
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        oracle.spmm_vbr_np(sample["payloads"], sample["row_perm"], sample["row_partition"], bounds, B64,
+                           threads=threads)
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def host_csr(dA):
+    return (dA.row_ptr.cpu().numpy(), dA.col_idx.cpu().numpy(), dA.values.cpu().numpy())
+
+
+def cpu_baseline(dA, bounds, dv, B, target_seconds, threads):
+    """Calibrate on a small sample, then time a sample sized for ~target_seconds."""
+    A_host = host_csr(dA)
+    B64 = B.float().cpu().numpy().astype(np.float64)
+    perm = dv.row_perm64.cpu().numpy()
+    rp, bp, bc = dv.host_structure()
+    gw = group_widths(bounds, rp, bp, bc)
+    N = B64.shape[1]
+    s = cpu_sample(A_host, bounds, perm, rp, gw, N, 2e9)
+    t = time_cpu(s, bounds, B64, threads)
+    target = min(2e9 / max(t, 1e-6) * target_seconds, 1e15)
+    s = cpu_sample(A_host, bounds, perm, rp, gw, N, target)
+    t = time_cpu(s, bounds, B64, threads)
+    useful = 2.0 * s["nnz"] * N
+    return {"value": useful / t / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "seconds": t,
+            "sample": f"oracle.spmm_vbr_np (numpy port of multiply.py:72-97, float64, per-block dgemm, "
+                      f"threads={threads}) on the first {s['rows']} permuted rows ({s['block_rows']} block rows, "
+                      f"{s['nnz']} nnz) of the same VBR structure and B"}
+
+
+# ---------------------------------------------------------------------------------------- main
+
+
+def build_workload(args, device):
+    from paper_2202_05868_b200 import synth
+    from paper_2202_05868_b200.device import DeviceVbr, block_1sa_device
+    from paper_2202_05868_b200.types import MergePolicy
+
+    t0 = time.perf_counter()
+    dA, bounds, cfg, meta = synth.make(args.config, scale=args.scale, device=device)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    pol = MergePolicy(tau=cfg.tau)
+    dg = block_1sa_device(dA, bounds, pol, True)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    dv = DeviceVbr.build(dA, bounds, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], dtypes=(cfg.precision,))
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    stages = {"synth_s": round(t1 - t0, 3), "block_1sa_s": round(t2 - t1, 4), "vbr_build_s": round(t3 - t2, 4),
+              "n_groups": dg.n_groups, "n_blocks": dv.n_blocks}
+    return dA, bounds, cfg, meta, dv, stages
+
+
+def run_ours(args, world, rank):
+    from paper_2202_05868_b200 import _lib as L
+    from paper_2202_05868_b200 import synth
+
+    device = torch.device("cuda", torch.cuda.current_device())
+    dA, bounds, cfg, meta, dv, stages = build_workload(args, device)
+    prec = cfg.precision
+    B = synth.make_b(cfg, dA.n_cols, prec, device=device)
+    N = cfg.N
+    C = torch.empty((dA.n_rows, N), dtype=torch.float32, device=device)
+    info = dv.plan_info(N, prec, rank, world)
+    launches_per_step = int(info["n_items_tall"] > 0) + int(info["n_items_short"] > 0) + int(info["n_items_simt"] > 0)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        dv.spmm(B, out=C, precision=prec, shard=rank, n_shards=world)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(torch.cuda.current_device())
+    barrier(world)
+    torch.cuda.synchronize()
+    with sampler:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            starts[k].record(stream)
+            dv.spmm(B, out=C, precision=prec, shard=rank, n_shards=world)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_local = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    ms = allreduce_max(ms_local, world)
+    useful = 2.0 * dA.nnz * N
+    value = useful / (ms * 1e-3) / 1e9
+
+    # ---- end to end through the reference-facing path: pinned float64 B -> device -> kernel -> float64 C
+    e2e = run_e2e(args, dv, dA, B, prec, rank, world)
+
+    peaks = measured_peaks()
+    achieved_tflops = useful / (ms_local * 1e-3) / 1e12 if world == 1 else useful / (ms * 1e-3) / 1e12
+    exec_tflops = info["executed_flops"] / (ms_local * 1e-3) / 1e12
+    roof = {"bound": "tensor", "kernel": "spmm_tall_kernel" if info["n_items_tall"] else "spmm_short_kernel",
+            "achieved": round(achieved_tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": round(achieved_tflops / peaks["bf16_tflops"], 5), "traffic": profile_traffic(args.config),
+            "peak_source": peaks["source"] + " (burst bf16, kernel timed alone)",
+            "algorithmic": "2*nnz*N flops per launch",
+            "executed_tflops": round(exec_tflops, 3),
+            "executed_frac": round(exec_tflops / peaks["bf16_tflops"], 4),
+            "executed_flops_per_launch": info["executed_flops"]}
+    if prec == "fp32":
+        roof.update(bound="hbm", kernel="spmm_simt_f32_kernel")
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+        "config": {"workload": f"config {cfg.name}: {cfg.description}", "n_rows": dA.n_rows, "n_cols": dA.n_cols,
+                   "nnz": dA.nnz, "N": N, "delta": cfg.delta, "tau": cfg.tau, "policy": "jaccard, bounded, update",
+                   "parallelism": f"block-row shards x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (256 MiB memset outside the timed events)"},
+        "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+        "clocks": sampler.summary(),
+        "stages": dict(stages, rho_prime=round(dA.nnz / max(dv.stored_area(), 1), 5),
+                       padding_executed_over_useful=round(info["executed_flops"] * world / useful, 3),
+                       padding_vbr_over_useful=round(info["vbr_flops"] * world / useful, 3)),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(dA, bounds, dv, B, args.cpu_seconds, os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_e2e(args, dv, dA, B, prec, rank, world):
+    """Steps through the reference-facing host path: H2D of the step's B (float64, pinned, as the
+    reference's DenseMatrix), conversion + SpMM on the device, D2H of C (float64, pinned)."""
+    from paper_2202_05868_b200 import _lib as L
+
+    N = B.shape[1]
+    K = B.shape[0]
+    B_host = B.double().cpu().pin_memory()
+    C_host = torch.empty((dA.n_rows, N), dtype=torch.float64).pin_memory()
+    dev = B.device
+    B_dev64 = torch.empty((K, N), dtype=torch.float64, device=dev)
+    ld = (N + 7) // 8 * 8
+    B_k = torch.empty((K, ld), dtype=L.TORCH_DTYPE[L.PRECISION[prec]], device=dev)
+    C32 = torch.empty((dA.n_rows, N), dtype=torch.float32, device=dev)
+    C64 = torch.empty((dA.n_rows, N), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    lib = L.lib()
+
+    def step():
+        B_dev64.copy_(B_host, non_blocking=True)
+        L.check(lib.rb_convert_f64(L.ptr(B_dev64), K, N, N, L.ptr(B_k), L.PRECISION[prec], ld, L.stream_handle()))
+        dv.spmm(B_k[:, :N], out=C32, precision=prec, shard=rank, n_shards=world)
+        L.check(lib.rb_widen_f32(L.ptr(C32), dA.n_rows, N, N, L.ptr(C64), N, L.stream_handle()))
+        C_host.copy_(C64, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = allreduce_max(s.elapsed_time(e) / args.e2e_steps, world)
+    return {"value": round(2.0 * dA.nnz * N / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(ms, 4),
+            "h2d_bytes_per_step": int(B_host.numel() * 8), "d2h_bytes_per_step": int(C_host.numel() * 8),
+            "path": "pinned float64 B -> H2D -> rb_convert_f64 -> rb_spmm_execute -> rb_widen_f32 -> D2H float64 C"}
+
+
+def run_reference(args, world, rank):
+    """The reference's CPU implementation of the path (numpy port, oracle/) on the host cores."""
+    if rank != 0:
+        return
+    from paper_2202_05868_b200 import synth
+
+    cuda = torch.cuda.is_available()
+    device = torch.device("cuda", torch.cuda.current_device()) if cuda else torch.device("cpu")
+    if cuda:
+        dA, bounds, cfg, meta, dv, stages = build_workload(args, device)
+        perm = dv.row_perm64.cpu().numpy()
+        rp, bp, bc = dv.host_structure()
+    else:  # structure from the oracle's 1-SA when no GPU is present
+        import oracle
+
+        dA, bounds, cfg, meta = synth.make(args.config, scale=args.scale, device="cpu")
+        s = oracle.block_1sa_arrays(dA.row_ptr.numpy(), dA.col_idx.numpy(), bounds, tau=cfg.tau)
+        perm, rp = s["row_perm"], s["group_ptr"]
+        bp, bc = oracle.vbr_blocks(dA.row_ptr.numpy(), dA.col_idx.numpy(), bounds, perm, rp)
+    gw = group_widths(bounds, rp, bp, bc)
+    B = synth.make_b(cfg, dA.n_cols, cfg.precision, device="cpu")
+    B64 = B.float().numpy().astype(np.float64)
+    threads = os.cpu_count() or 1
+    A_host = host_csr(dA)
+    per_step = min(2.0, 150.0 / max(1, args.steps + args.warmup))
+    N = B64.shape[1]
+    cal = cpu_sample(A_host, bounds, perm, rp, gw, N, 2e9)
+    t = time_cpu(cal, bounds, B64, threads)
+    sample = cpu_sample(A_host, bounds, perm, rp, gw, N, 2e9 / max(t, 1e-6) * per_step)
+    for _ in range(args.warmup):
+        time_cpu(sample, bounds, B64, threads)
+    times = [time_cpu(sample, bounds, B64, threads) for _ in range(args.steps)]
+    ms = 1e3 * float(np.mean(times))
+    value = 2.0 * sample["nnz"] * B64.shape[1] / (ms * 1e-3) / 1e9
+    desc = (f"oracle.spmm_vbr_np (numpy port of multiply.py:72-97, float64 per-block dgemm, threads={threads}) "
+            f"on the first {sample['rows']} permuted rows ({sample['nnz']} nnz) per step")
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"config {cfg.name}: {cfg.description}", "n_rows": dA.n_rows, "n_cols": dA.n_cols,
+                      "nnz": dA.nnz, "N": cfg.N, "delta": cfg.delta, "tau": cfg.tau},
+           "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                            "sample": desc},
+           "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py --impl ours needs a CUDA device")
+        run_ours(args, world, rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
