@@ -152,6 +152,13 @@ int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t 
 int rb_spmm_plan_info(const rb_spmm_plan* plan, rb_spmm_info* info);
 int rb_spmm_execute(const rb_spmm_plan* plan, const void* B, int64_t ldb, float* C, int64_t ldc, void* stream);
 int rb_spmm_plan_destroy(rb_spmm_plan* plan);
+/* Host-only shard planner (no device access): the contiguous range [*row_begin, *row_end) of
+ * PERMUTED row positions owned by `shard`, given HOST copies of row_partition / blk_ptr.
+ * rb_spmm_plan_create(..., shard, n_shards, ...) uses exactly this range; C rows
+ * row_perm[row_begin:row_end] are produced by that shard and by no other.            */
+int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* blk_ptr, int64_t n_block_rows,
+                        int32_t b_dtype, int32_t dp, int32_t shard, int32_t n_shards, int64_t* row_begin,
+                        int64_t* row_end);
 
 /* ------------------------------------------------------------------ helpers
  * Element conversion used by the drop-in path (DenseMatrix is float64, matrix.py:107-111):

@@ -354,6 +354,61 @@ static int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt
   return RB_OK;
 }
 
+// Shard = contiguous range of permuted rows, cut at work-unit boundaries so that every C row
+// (and every work item) belongs to exactly one shard.  Units: (block row, 128-row M-tile) for tall
+// block rows, whole short block rows, (block row, 8-row chunk) on the fp32 path; weight = padded
+// MMA work (blocks x K chunks + 1) x rows.  A unit goes to the shard owning its weight midpoint.
+int shard_range(const int32_t* rp, const int32_t* bp, int64_t H, int32_t b_dtype, int32_t dp, int32_t shard,
+                int32_t n_shards, int64_t* row_lo, int64_t* row_hi) {
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(RB_EINVAL, "bad shard");
+  const bool tc = (b_dtype == RB_BF16 || b_dtype == RB_F16);
+  const int dpc = tc ? std::max(1, dp / KCH) : 1;
+  struct Unit {
+    int64_t r0, r1;
+    double w;
+  };
+  std::vector<Unit> units;
+  units.reserve(H);
+  double total = 0;
+  for (int64_t g = 0; g < H; ++g) {
+    const int h = rp[g + 1] - rp[g];
+    const int nb = bp[g + 1] - bp[g];
+    if (h <= 0) continue;
+    const int step = !tc ? SIMT_ROWS : is_short_row(h) ? h : TALL_BM;
+    for (int r = 0; r < h; r += step) {
+      const int rows = std::min(step, h - r);
+      const double w = (nb * (double)dpc + 1.0) * (tc ? (is_short_row(h) ? hp_of(h) : TALL_BM) : rows);
+      units.push_back({rp[g] + r, rp[g] + r + rows, w});
+      total += w;
+    }
+  }
+  const double lo = total * shard / n_shards, hi = total * (shard + 1) / n_shards;
+  double acc = 0;
+  int64_t a = -1, b = -1;
+  for (auto& u : units) {
+    const double mid = acc + 0.5 * u.w;
+    acc += u.w;
+    const bool mine = mid >= lo && (mid < hi || shard == n_shards - 1);
+    if (mine) {
+      if (a < 0) a = u.r0;
+      b = u.r1;
+    }
+  }
+  if (a < 0) {  // empty shard: an empty range positioned after the previous shards
+    int64_t pos = 0;
+    acc = 0;
+    for (auto& u : units) {
+      const double mid = acc + 0.5 * u.w;
+      acc += u.w;
+      if (mid < lo) pos = u.r1;
+    }
+    a = b = pos;
+  }
+  *row_lo = a;
+  *row_hi = b;
+  return RB_OK;
+}
+
 }  // namespace rb
 
 struct rb_spmm_plan {
@@ -387,56 +442,37 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
     RB_CUDA_TRY(cudaMemcpyAsync(bp.data(), vbr->blk_ptr, sizeof(int32_t) * (H + 1), cudaMemcpyDeviceToHost, stream));
     RB_CUDA_TRY(cudaStreamSynchronize(stream));
   }
-  // Work units = (block row, row chunk); all column chunks of a unit stay together so each C
-  // row belongs to exactly one shard.  Weight = (blocks + 1) x rows-of-MMA x columns.
-  struct Unit {
-    int32_t g, sub, kind;  // kind 0 tall, 1 short, 2 simt
-    double w;
-  };
-  std::vector<Unit> units;
-  units.reserve(H);
-  const int dpc = tc ? vbr->dp / KCH : 1;
+  int64_t row_lo = 0, row_hi = 0;
+  {
+    int rc = shard_range(rp.data(), bp.data(), H, b_dtype, vbr->dp, shard, n_shards, &row_lo, &row_hi);
+    if (rc) return rc;
+  }
+  std::vector<int4> tall, shrt, simt;
+  int64_t first_row = row_lo < row_hi ? row_lo : -1;
+  double exec_flops = 0, vbr_flops = 0;
+  const int64_t Npad = (N + 15) / 16 * 16;
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
-    if (h <= 0) continue;
+    if (h <= 0 || rp[g + 1] <= row_lo || rp[g] >= row_hi) continue;
     if (!tc) {
-      for (int r0 = 0; r0 < h; r0 += SIMT_ROWS) units.push_back({(int32_t)g, r0, 2, (nb + 1.0) * SIMT_ROWS});
+      for (int r0 = 0; r0 < h; r0 += SIMT_ROWS) {
+        if (rp[g] + r0 < row_lo || rp[g] + r0 >= row_hi) continue;
+        for (int64_t n0 = 0; n0 < N; n0 += SIMT_COLS) simt.push_back(make_int4((int)g, r0, (int)n0, nb));
+        exec_flops += 2.0 * nb * std::min(SIMT_ROWS, h - r0) * (double)vbr->dp * N;
+        vbr_flops += 2.0 * nb * std::min(SIMT_ROWS, h - r0) * (double)vbr->dp * N;
+      }
     } else if (is_short_row(h)) {
-      units.push_back({(int32_t)g, 0, 1, (nb * dpc + 1.0) * 128.0 * 0.5 * (hp_of(h) / 16 + 1)});
-    } else {
-      for (int m = 0; m < (h + TALL_BM - 1) / TALL_BM; ++m)
-        units.push_back({(int32_t)g, m, 0, (nb * dpc + 1.0) * 256.0});
-    }
-  }
-  double total = 0;
-  for (auto& u : units) total += u.w;
-  const double lo = total * shard / n_shards, hi = total * (shard + 1) / n_shards;
-  std::vector<int4> tall, shrt, simt;
-  double acc = 0;
-  int64_t first_row = -1;
-  double exec_flops = 0, vbr_flops = 0;
-  const int64_t Npad = (N + 15) / 16 * 16;
-  for (auto& u : units) {
-    const double mid = acc + 0.5 * u.w;  // unit goes to the shard owning its midpoint
-    acc += u.w;
-    if (!(mid >= lo && (mid < hi || (shard == n_shards - 1 && mid <= hi)))) continue;
-    const int g = u.g;
-    const int h = rp[g + 1] - rp[g];
-    const int nb = bp[g + 1] - bp[g];
-    if (first_row < 0) first_row = rp[g] + (u.kind == 0 ? u.sub * TALL_BM : u.kind == 2 ? u.sub : 0);
-    if (u.kind == 0) {
-      for (int64_t n0 = 0; n0 < N; n0 += TALL_BN) tall.push_back(make_int4(g, u.sub, (int)n0, nb));
-      exec_flops += 2.0 * nb * TALL_BM * vbr->dp * Npad;
-      vbr_flops += 2.0 * nb * std::min(TALL_BM, h - u.sub * TALL_BM) * (double)vbr->dp * N;
-    } else if (u.kind == 1) {
-      for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS) shrt.push_back(make_int4(g, hp_of(h), (int)n0, nb));
+      for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS) shrt.push_back(make_int4((int)g, hp_of(h), (int)n0, nb));
       exec_flops += 2.0 * nb * hp_of(h) * vbr->dp * ((N + 127) / 128 * 128);
       vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
     } else {
-      for (int64_t n0 = 0; n0 < N; n0 += SIMT_COLS) simt.push_back(make_int4(g, u.sub, (int)n0, nb));
-      exec_flops += 2.0 * nb * std::min(SIMT_ROWS, h - u.sub) * (double)vbr->dp * N;
-      vbr_flops += 2.0 * nb * std::min(SIMT_ROWS, h - u.sub) * (double)vbr->dp * N;
+      for (int m = 0; m < (h + TALL_BM - 1) / TALL_BM; ++m) {
+        if (rp[g] + m * TALL_BM < row_lo || rp[g] + m * TALL_BM >= row_hi) continue;
+        for (int64_t n0 = 0; n0 < N; n0 += TALL_BN) tall.push_back(make_int4((int)g, m, (int)n0, nb));
+        exec_flops += 2.0 * nb * TALL_BM * vbr->dp * Npad;
+        vbr_flops += 2.0 * nb * std::min(TALL_BM, h - m * TALL_BM) * (double)vbr->dp * N;
+      }
     }
   }
   // Longest-first order for the tensor-core kernels (LPT against the tail), stable.
@@ -567,4 +603,11 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
     RB_CUDA_TRY(cudaGetLastError());
   }
   return RB_OK;
+}
+
+extern "C" int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* blk_ptr, int64_t n_block_rows,
+                                   int32_t b_dtype, int32_t dp, int32_t shard, int32_t n_shards, int64_t* row_begin,
+                                   int64_t* row_end) {
+  if (!row_partition || !blk_ptr || !row_begin || !row_end || n_block_rows < 0) return fail(RB_EINVAL, "bad arguments");
+  return shard_range(row_partition, blk_ptr, n_block_rows, b_dtype, dp, shard, n_shards, row_begin, row_end);
 }
