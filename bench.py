@@ -299,7 +299,7 @@ def run_ours(args, world, rank):
     peaks = measured_peaks()
     achieved_tflops = useful / (ms_local * 1e-3) / 1e12 if world == 1 else useful / (ms * 1e-3) / 1e12
     exec_tflops = info["executed_flops"] / (ms_local * 1e-3) / 1e12
-    roof = {"bound": "tensor", "kernel": "spmm_tall_kernel" if info["n_items_tall"] else "spmm_short_kernel",
+    roof = {"bound": "tensor", "kernel": "spmm_tall2_kernel" if info["n_items_tall"] else "spmm_short2_kernel",
             "achieved": round(achieved_tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": round(achieved_tflops / peaks["bf16_tflops"], 5), "traffic": profile_traffic(args.config),
             "peak_source": peaks["source"] + " (burst bf16, kernel timed alone)",

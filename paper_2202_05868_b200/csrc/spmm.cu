@@ -1,19 +1,26 @@
 // VBR x dense SpMM on sm_100a: TMA -> SMEM -> tcgen05.mma (bf16/fp16 in, fp32 accumulate in
 // TMEM) -> tcgen05.ld -> un-permuted C rows.  Replaces spmm_vbr (multiply.py:72-97).
 //
-// Two tensor-core kernels share one pipeline skeleton (warp 0 lane 0 = TMA producer,
-// warp 1 lane 0 = MMA issuer, all 4 warps = epilogue):
-//   spmm_tall_kernel   block rows with h > 128: D[128 rows x 256 cols] per work item,
-//                      A = tile rows (K-major, SW128), B = B panel (MN-major, SW128).
-//   spmm_short_kernel  block rows with h <= 128 (swap-AB): D^T[256 cols x hp rows],
-//                      MMA A = B panel (MN-major), MMA B = tile rows (K-major), N = hp.
-// The K loop of a work item runs over the block row's stored blocks (ascending bcol) and
-// the 64-wide K chunks of each block; the B panel of block (g, bcol) is rows
-// col_bounds[bcol] .. +64 of B.  Tile columns beyond the segment width are zero, so B rows
-// of the neighbouring segment (or TMA zero fill past n_cols) contribute exactly 0.
+// Both tensor-core kernels are persistent and warp specialised (192 threads):
+//   warp 0 lane 0  TMA producer (mbarrier ring of SMEM stages)
+//   warp 1         TMEM allocator; lane 0 issues tcgen05.mma (leader CTA only for 2-CTA)
+//   warps 2..5     epilogue: tcgen05.ld (32 lanes x 32b) -> C rows at row_perm positions
+// with two TMEM accumulators (2 x 256 columns) so the epilogue of work item i overlaps the
+// MMAs of item i+1.
+//
+//   spmm_tall2_kernel   block rows with h > 128, CTA pair (cta_group::2): D = 256 rows x 256
+//                       cols; each CTA stages its 128 A-tile rows (K-major, SW128) and its
+//                       128-column half of the B panel (MN-major, SW128); the leader issues
+//                       tcgen05.mma.cta_group::2 M=256 N=256 K=16.
+//   spmm_short2_kernel  block rows with h <= 128 (swap-AB): D^T = Bpanel^T (MN-major, M = 128 C
+//                       columns, two M-tiles per item) x tile^T (K-major, N = hp rows).
+// The K loop of an item runs over the block row's stored blocks (ascending bcol) and their 64-wide
+// K chunks; the B panel of block (g, bcol) is rows col_bounds[bcol] .. +64.  Tile columns past the
+// segment width are zero, so neighbouring-segment B rows (or TMA zero fill past n_cols) add 0.
 //
 // spmm_simt_f32_kernel is the fp32 check path (tcgen05 has no fp32-exact MMA).
 #include <algorithm>
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <vector>
@@ -23,16 +30,28 @@
 
 namespace rb {
 
-constexpr int KCH = 64;                       // K elements per pipeline stage (one SW128 row)
-constexpr int STAGES = 4;
-constexpr int TALL_BM = 128;
+constexpr int KCH = 64;                      // K elements per pipeline stage (one SW128 row)
+constexpr int TC_THREADS = 192;
+constexpr uint32_t BOX_BYTES = 64 * 64 * 2;  // one [64 k x 64 n] B box (8 KB)
+constexpr int ACC_COLS = 256;                // TMEM columns per accumulator (x2 buffers)
+
+// tall (2-CTA)
+constexpr int PAIR_BM = 256;                 // rows of a tall work item (2 CTAs x 128)
 constexpr int TALL_BN = 256;
-constexpr int SHORT_NS = 256;                 // C columns per short work item (2 x M=128)
-constexpr uint32_t BOX_BYTES = 64 * 64 * 2;   // one [64 k x 64 n] B box
-constexpr uint32_t A_SLOT = 128 * KCH * 2;    // 16 KB
-constexpr uint32_t B_SLOT = KCH * 256 * 2;    // 32 KB
-constexpr uint32_t STAGE_BYTES = A_SLOT + B_SLOT;
-constexpr uint32_t SMEM_TC = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int T_STAGES = 6;
+constexpr uint32_t T_A_BYTES = 128 * KCH * 2;           // 16 KB: this CTA's 128 A rows
+constexpr uint32_t T_B_BYTES = 2 * BOX_BYTES;           // 16 KB: this CTA's 128 B columns
+constexpr uint32_t T_STAGE = T_A_BYTES + T_B_BYTES;     // 32 KB
+constexpr uint32_t SMEM_TALL = T_STAGES * T_STAGE + 1024 + 256;
+
+// short (swap-AB, 1 CTA)
+constexpr int SHORT_NS = 256;                // C columns per item (2 x M=128)
+constexpr int S_STAGES = 4;
+constexpr uint32_t S_A_SLOT = 128 * KCH * 2;            // up to 128 tile rows
+constexpr uint32_t S_B_BYTES = 4 * BOX_BYTES;           // 64 k x 256 n
+constexpr uint32_t S_STAGE = S_A_SLOT + S_B_BYTES;      // 48 KB
+constexpr uint32_t SMEM_SHORT = S_STAGES * S_STAGE + 1024 + 256;
+
 constexpr int SIMT_ROWS = 8;
 constexpr int SIMT_COLS = 128;
 
@@ -49,11 +68,18 @@ struct SpmmArgs {
   float* C;
   int64_t ldc;
   int32_t N;
-  uint32_t ab_fmt;  // 0 = f16, 1 = bf16
+  uint32_t ab_fmt;      // 0 = f16, 1 = bf16
+  uint32_t a_evict_first;  // L2 policy of A-tile loads: 1 = evict_first, 0 = evict_normal
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void store_row_chunk(float* dst, const uint32_t (&r)[32], int ncols, bool vec) {
@@ -71,221 +97,322 @@ __device__ __forceinline__ void store_row_chunk(float* dst, const uint32_t (&r)[
   }
 }
 
+struct PipeState {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void advance(int stages) {
+    if (++s == stages) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+};
+
 // ------------------------------------------------------------------------------------------
-// tall block rows: one CTA per (g, m_tile, n0); D = 128 x 256 fp32 in TMEM (256 columns).
-__global__ void __launch_bounds__(128, 1)
-    spmm_tall_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     SpmmArgs a) {
+// tall block rows, CTA pair.  Item = (g, 256-row pair tile m, n0).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    spmm_tall2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      SpmmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE);
+  uint64_t* empty = full + T_STAGES;
+  uint64_t* tfull = empty + T_STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int4 it = a.items[blockIdx.x];
-  const int g = it.x, m_tile = it.y, n0 = it.z;
-  const int p0 = a.row_partition[g];
-  const int h = a.row_partition[g + 1] - p0;
-  const int hp = hp_of(h);
-  const int b_begin = a.blk_ptr[g];
-  const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
-  const int n_mma = min(TALL_BN, (a.N - n0 + 15) / 16 * 16);
-  const uint32_t idesc = idesc_f16(128, n_mma, a.ab_fmt, /*a_mn=*/0, /*b_mn=*/1);
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < T_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0 && nk > 0) {
-    // ---------------- TMA producer
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    const int64_t tile_row0 = a.grp_tile_row[g] + (int64_t)m_tile * TALL_BM;
-    const int n_boxes = min(4, (a.N - n0 + 63) / 64);
-    const uint32_t tx = A_SLOT + n_boxes * BOX_BYTES;
-    for (int k = 0; k < nk; ++k) {
-      const int s = k % STAGES;
-      if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) & 1) ^ 1);
-      const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
-      const int bcol = a.blk_col[b_begin + t];
-      uint8_t* sA = smem + s * STAGE_BYTES;
-      uint8_t* sB = sA + A_SLOT;
-      mbar_arrive_expect_tx(&full[s], tx);
-      tma_load_2d(sA, &tmA, &full[s], kc * KCH, (int32_t)(tile_row0 + (int64_t)t * hp));
-      const int krow = a.col_bounds[bcol] + kc * KCH;
-      for (int i = 0; i < n_boxes; ++i) tma_load_2d(sB + i * BOX_BYTES, &tmB, &full[s], n0 + 64 * i, krow);
-    }
-  } else if (warp == 1 && lane == 0 && nk > 0) {
-    // ---------------- MMA issuer (single thread)
-    for (int k = 0; k < nk; ++k) {
-      const int s = k % STAGES;
-      mbar_wait(&full[s], (k / STAGES) & 1);
-      tc_fence_after();
-      const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
-      const uint32_t b_base = a_base + A_SLOT;
-#pragma unroll
-      for (int kk = 0; kk < KCH / 16; ++kk) {
-        const uint64_t ad = sdesc_sw128(a_base + kk * 32, 16, 1024);       // K-major, +16 elems = 32 B
-        const uint64_t bd = sdesc_sw128(b_base + kk * 2048, BOX_BYTES, 1024);  // MN-major, +16 rows
-        umma_f16(tmem, ad, bd, idesc, (k | kk) != 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs; bytes land on the leader's full barrier)
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      const uint64_t pol_a = a.a_evict_first ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_b = policy_evict_last();
+      PipeState ps;
+      for (int i = pair; i < a.n_items; i += n_pairs) {
+        const int4 it = a.items[i];
+        const int g = it.x, m = it.y, n0 = it.z;
+        const int h = a.row_partition[g + 1] - a.row_partition[g];
+        const int hp = hp_of(h);
+        const int b_begin = a.blk_ptr[g];
+        const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
+        const int64_t row0 = a.grp_tile_row[g] + (int64_t)m * PAIR_BM + rank * 128;
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(&empty[ps.s], ps.ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[ps.s], 2 * T_STAGE);
+          const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
+          const int bcol = a.blk_col[b_begin + t];
+          uint8_t* sA = smem + ps.s * T_STAGE;
+          uint8_t* sB = sA + T_A_BYTES;
+          tma_load_2d_2sm(sA, &tmA, &full[ps.s], kc * KCH, (int32_t)(row0 + (int64_t)t * hp), pol_a);
+          const int krow = a.col_bounds[bcol] + kc * KCH;
+          const int nb0 = n0 + (int)rank * 128;
+          tma_load_2d_2sm(sB, &tmB, &full[ps.s], nb0, krow, pol_b);
+          tma_load_2d_2sm(sB + BOX_BYTES, &tmB, &full[ps.s], nb0 + 64, krow, pol_b);
+          ps.advance(T_STAGES);
+        }
       }
-      umma_commit(&empty[s]);
+      // drain: every stage's last MMA commit has landed before teardown
+      for (int k = 0; k < T_STAGES; ++k) {
+        mbar_wait(&empty[ps.s], ps.ph ^ 1);
+        ps.advance(T_STAGES);
+      }
     }
-    umma_commit(tfull);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM lane = tile row, 32 fp32 columns per tcgen05.ld
-  if (nk > 0) {
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-  }
-  const int row_local = m_tile * TALL_BM + warp * 32 + lane;
-  const bool valid = row_local < h;
-  const int64_t crow = valid ? (int64_t)a.row_perm[p0 + row_local] : 0;
-  float* dst = a.C + crow * a.ldc + n0;
-  const bool vec = ((a.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
-  const int ncol = min(TALL_BN, a.N - n0);
-  for (int c = 0; c < ncol; c += 32) {
-    uint32_t r[32];
-    if (nk > 0) {
-      tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
-      tmem_ld_wait();
-    } else {
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader CTA, one thread)
+      const uint32_t idesc = idesc_f16(256, TALL_BN, a.ab_fmt, /*a_mn=*/0, /*b_mn=*/1);
+      PipeState ps;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int i = pair; i < a.n_items; i += n_pairs) {
+        const int g = a.items[i].x;
+        const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
+        if (nk == 0) continue;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(&full[ps.s], ps.ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + ps.s * T_STAGE);
+          const uint32_t b_base = a_base + T_A_BYTES;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) r[j] = 0u;
+          for (int kk = 0; kk < KCH / 16; ++kk) {
+            const uint64_t ad = sdesc_sw128(a_base + kk * 32, 16, 1024);            // K-major: +16 elems
+            const uint64_t bd = sdesc_sw128(b_base + kk * 2048, BOX_BYTES, 1024);   // MN-major: +16 rows
+            umma_f16_2sm(d, ad, bd, idesc, (k | kk) != 0);
+          }
+          umma_commit_2sm_mc(&empty[ps.s], 0x3);
+          ps.advance(T_STAGES);
+        }
+        umma_commit_2sm_mc(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
     }
-    if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+  } else {
+    // ---------------- epilogue (both CTAs): TMEM lane = row rank*128 + 32q + lane of the pair tile
+    const int q = warp & 3;
+    const bool vec = ((a.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int i = pair; i < a.n_items; i += n_pairs) {
+      const int4 it = a.items[i];
+      const int g = it.x, m = it.y, n0 = it.z;
+      const int p0 = a.row_partition[g];
+      const int h = a.row_partition[g + 1] - p0;
+      const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
+      const int row_local = m * PAIR_BM + (int)rank * 128 + q * 32 + lane;
+      const bool valid = row_local < h;
+      const int64_t crow = valid ? (int64_t)a.row_perm[p0 + row_local] : 0;
+      float* dst = a.C + crow * a.ldc + n0;
+      const int ncol = min(TALL_BN, a.N - n0);
+      if (nk > 0) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
+      for (int c = 0; c < ncol; c += 32) {
+        uint32_t r[32];
+        if (nk > 0) {
+          tmem_ld_32x32b_x32(tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16) + c, r);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
+        if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+      }
+      if (nk > 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<256>(tmem);
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_2sm<512>(tmem);
 }
 
 // ------------------------------------------------------------------------------------------
-// short block rows (swap-AB): one CTA per (g, n0); D_mt^T = B[:, n0+128mt .. +128]^T x tile^T,
-// M = 128 C columns, N = hp tile rows.  TMEM columns [mt*hp, mt*hp + hp).
-__global__ void __launch_bounds__(128, 1)
-    spmm_short_kernel(const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
-                      const __grid_constant__ CUtensorMap tmA64, const __grid_constant__ CUtensorMap tmA128,
-                      const __grid_constant__ CUtensorMap tmB, SpmmArgs a) {
+// short block rows (swap-AB), one CTA.  Item = (g, hp, n0).  D_mt^T[128 C cols x hp rows] at TMEM
+// columns acc*256 + mt*hp.
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    spmm_short2_kernel(const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
+                       const __grid_constant__ CUtensorMap tmA64, const __grid_constant__ CUtensorMap tmA128,
+                       const __grid_constant__ CUtensorMap tmB, SpmmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_STAGES * S_STAGE);
+  uint64_t* empty = full + S_STAGES;
+  uint64_t* tfull = empty + S_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int4 it = a.items[blockIdx.x];
-  const int g = it.x, n0 = it.z;
-  const int p0 = a.row_partition[g];
-  const int h = a.row_partition[g + 1] - p0;
-  const int hp = hp_of(h);
-  const int b_begin = a.blk_ptr[g];
-  const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
-  const int n_mt = min(2, (a.N - n0 + 127) / 128);
-  const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < S_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0 && nk > 0) {
-    const CUtensorMap* tmA = hp == 16 ? &tmA16 : hp == 32 ? &tmA32 : hp == 64 ? &tmA64 : &tmA128;
-    tma_prefetch_desc(tmA);
-    tma_prefetch_desc(&tmB);
-    const int64_t tile_row0 = a.grp_tile_row[g];
-    const int n_boxes = min(4, (a.N - n0 + 63) / 64);
-    const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
-    for (int k = 0; k < nk; ++k) {
-      const int s = k % STAGES;
-      if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) & 1) ^ 1);
-      const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
-      const int bcol = a.blk_col[b_begin + t];
-      uint8_t* sA = smem + s * STAGE_BYTES;
-      uint8_t* sB = sA + A_SLOT;
-      mbar_arrive_expect_tx(&full[s], tx);
-      tma_load_2d(sA, tmA, &full[s], kc * KCH, (int32_t)(tile_row0 + (int64_t)t * hp));
-      const int krow = a.col_bounds[bcol] + kc * KCH;
-      for (int i = 0; i < n_boxes; ++i) tma_load_2d(sB + i * BOX_BYTES, &tmB, &full[s], n0 + 64 * i, krow);
-    }
-  } else if (warp == 1 && lane == 0 && nk > 0) {
-    for (int k = 0; k < nk; ++k) {
-      const int s = k % STAGES;
-      mbar_wait(&full[s], (k / STAGES) & 1);
-      tc_fence_after();
-      const uint32_t t_base = smem_u32(smem + s * STAGE_BYTES);  // tile rows (K-major)
-      const uint32_t b_base = t_base + A_SLOT;                    // B panel (MN-major)
-      for (int mt = 0; mt < n_mt; ++mt) {
-#pragma unroll
-        for (int kk = 0; kk < KCH / 16; ++kk) {
-          const uint64_t ad = sdesc_sw128(b_base + mt * 2 * BOX_BYTES + kk * 2048, BOX_BYTES, 1024);
-          const uint64_t bd = sdesc_sw128(t_base + kk * 32, 16, 1024);
-          umma_f16(tmem + mt * hp, ad, bd, idesc, (k | kk) != 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmB);
+      const uint64_t pol_a = a.a_evict_first ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_b = policy_evict_last();
+      PipeState ps;
+      for (int i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+        const int4 it = a.items[i];
+        const int g = it.x, hp = it.y, n0 = it.z;
+        const CUtensorMap* tmA = hp == 16 ? &tmA16 : hp == 32 ? &tmA32 : hp == 64 ? &tmA64 : &tmA128;
+        const int b_begin = a.blk_ptr[g];
+        const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
+        const int64_t row0 = a.grp_tile_row[g];
+        const int n_boxes = min(4, (a.N - n0 + 63) / 64);
+        const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(&empty[ps.s], ps.ph ^ 1);
+          mbar_arrive_expect_tx(&full[ps.s], tx);
+          const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
+          const int bcol = a.blk_col[b_begin + t];
+          uint8_t* sA = smem + ps.s * S_STAGE;
+          uint8_t* sB = sA + S_A_SLOT;
+          tma_load_2d_hint(sA, tmA, &full[ps.s], kc * KCH, (int32_t)(row0 + (int64_t)t * hp), pol_a);
+          const int krow = a.col_bounds[bcol] + kc * KCH;
+          for (int bx = 0; bx < n_boxes; ++bx)
+            tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[ps.s], n0 + 64 * bx, krow, pol_b);
+          ps.advance(S_STAGES);
         }
       }
-      umma_commit(&empty[s]);
-    }
-    umma_commit(tfull);
-  }
-  __syncwarp();
-
-  if (nk > 0) {
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-  }
-  // epilogue: TMEM lane = C column, TMEM column = block-row row; a warp stores 32 consecutive
-  // columns of one C row per instruction (coalesced 128 B).
-  for (int mt = 0; mt < 2; ++mt) {
-    const int n = n0 + mt * 128 + warp * 32 + lane;
-    const bool nvalid = n < a.N;
-    if (mt >= n_mt) break;
-    for (int j0 = 0; j0 < h; j0 += 16) {
-      uint32_t r[16];
-      if (nk > 0) {
-        tmem_ld_32x32b_x16(tmem + ((uint32_t)(warp * 32) << 16) + mt * hp + j0, r);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) r[j] = 0u;
+      for (int k = 0; k < S_STAGES; ++k) {
+        mbar_wait(&empty[ps.s], ps.ph ^ 1);
+        ps.advance(S_STAGES);
       }
-      if (nvalid) {
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      PipeState ps;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+        const int4 it = a.items[i];
+        const int g = it.x, hp = it.y, n0 = it.z;
+        const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
+        if (nk == 0) continue;
+        const int n_mt = min(2, (a.N - n0 + 127) / 128);
+        const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(&full[ps.s], ps.ph);
+          tc_fence_after();
+          const uint32_t t_base = smem_u32(smem + ps.s * S_STAGE);  // tile rows (K-major)
+          const uint32_t b_base = t_base + S_A_SLOT;                 // B panel (MN-major)
+          for (int mt = 0; mt < n_mt; ++mt) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j0 + j < h) {
-            const int64_t crow = a.row_perm[p0 + j0 + j];
-            a.C[crow * a.ldc + n] = __uint_as_float(r[j]);
+            for (int kk = 0; kk < KCH / 16; ++kk) {
+              const uint64_t ad = sdesc_sw128(b_base + mt * 2 * BOX_BYTES + kk * 2048, BOX_BYTES, 1024);
+              const uint64_t bd = sdesc_sw128(t_base + kk * 32, 16, 1024);
+              umma_f16(d + mt * hp, ad, bd, idesc, (k | kk) != 0);
+            }
+          }
+          umma_commit(&empty[ps.s]);
+          ps.advance(S_STAGES);
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // epilogue: TMEM lane = C column, column = block-row row; a warp stores 32 consecutive floats
+    // (128 B) of one C row per instruction
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+      const int4 it = a.items[i];
+      const int g = it.x, hp = it.y, n0 = it.z;
+      const int p0 = a.row_partition[g];
+      const int h = a.row_partition[g + 1] - p0;
+      const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
+      const int n_mt = min(2, (a.N - n0 + 127) / 128);
+      if (nk > 0) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
+      for (int mt = 0; mt < n_mt; ++mt) {
+        const int n = n0 + mt * 128 + q * 32 + lane;
+        const bool nvalid = n < a.N;
+        for (int j0 = 0; j0 < h; j0 += 16) {
+          uint32_t r[16];
+          if (nk > 0) {
+            tmem_ld_32x32b_x16(tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16) + mt * hp + j0, r);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = 0u;
+          }
+          if (nvalid) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j0 + j < h) a.C[(int64_t)a.row_perm[p0 + j0 + j] * a.ldc + n] = __uint_as_float(r[j]);
+            }
           }
         }
+      }
+      if (nk > 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<256>(tmem);
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -354,10 +481,13 @@ static int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt
   return RB_OK;
 }
 
-// Shard = contiguous range of permuted rows, cut at work-unit boundaries so that every C row
-// (and every work item) belongs to exactly one shard.  Units: (block row, 128-row M-tile) for tall
-// block rows, whole short block rows, (block row, 8-row chunk) on the fp32 path; weight = padded
-// MMA work (blocks x K chunks + 1) x rows.  A unit goes to the shard owning its weight midpoint.
+// Work unit of the shard planner: rows of one tall pair tile (256), a whole short block row, or an
+// 8-row chunk on the fp32 path.
+static int unit_rows(bool tc, int h) { return !tc ? SIMT_ROWS : is_short_row(h) ? h : PAIR_BM; }
+
+// Shard = contiguous range of permuted rows, cut at work-unit boundaries so that every C row (and
+// every work item) belongs to exactly one shard.  Weight = padded MMA work (K chunks + 1) x rows;
+// a unit goes to the shard owning its weight midpoint.
 int shard_range(const int32_t* rp, const int32_t* bp, int64_t H, int32_t b_dtype, int32_t dp, int32_t shard,
                 int32_t n_shards, int64_t* row_lo, int64_t* row_hi) {
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(RB_EINVAL, "bad shard");
@@ -374,38 +504,30 @@ int shard_range(const int32_t* rp, const int32_t* bp, int64_t H, int32_t b_dtype
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
     if (h <= 0) continue;
-    const int step = !tc ? SIMT_ROWS : is_short_row(h) ? h : TALL_BM;
+    const int step = unit_rows(tc, h);
     for (int r = 0; r < h; r += step) {
       const int rows = std::min(step, h - r);
-      const double w = (nb * (double)dpc + 1.0) * (tc ? (is_short_row(h) ? hp_of(h) : TALL_BM) : rows);
+      const double w = (nb * (double)dpc + 1.0) * (tc ? (is_short_row(h) ? hp_of(h) : PAIR_BM) : rows);
       units.push_back({rp[g] + r, rp[g] + r + rows, w});
       total += w;
     }
   }
   const double lo = total * shard / n_shards, hi = total * (shard + 1) / n_shards;
   double acc = 0;
-  int64_t a = -1, b = -1;
+  int64_t first = -1, last = -1, before = 0;
   for (auto& u : units) {
     const double mid = acc + 0.5 * u.w;
     acc += u.w;
+    if (mid < lo) before = u.r1;
     const bool mine = mid >= lo && (mid < hi || shard == n_shards - 1);
     if (mine) {
-      if (a < 0) a = u.r0;
-      b = u.r1;
+      if (first < 0) first = u.r0;
+      last = u.r1;
     }
   }
-  if (a < 0) {  // empty shard: an empty range positioned after the previous shards
-    int64_t pos = 0;
-    acc = 0;
-    for (auto& u : units) {
-      const double mid = acc + 0.5 * u.w;
-      acc += u.w;
-      if (mid < lo) pos = u.r1;
-    }
-    a = b = pos;
-  }
-  *row_lo = a;
-  *row_hi = b;
+  if (first < 0) first = last = before;  // empty shard: empty range after the previous shards
+  *row_lo = first;
+  *row_hi = last;
   return RB_OK;
 }
 
@@ -422,6 +544,13 @@ struct rb_spmm_plan {
 };
 
 using namespace rb;
+
+extern "C" int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* blk_ptr, int64_t n_block_rows,
+                                   int32_t b_dtype, int32_t dp, int32_t shard, int32_t n_shards, int64_t* row_begin,
+                                   int64_t* row_end) {
+  if (!row_partition || !blk_ptr || !row_begin || !row_end || n_block_rows < 0) return fail(RB_EINVAL, "bad arguments");
+  return shard_range(row_partition, blk_ptr, n_block_rows, b_dtype, dp, shard, n_shards, row_begin, row_end);
+}
 
 extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
                                    int32_t n_shards, rb_spmm_plan** out, void* stream_) {
@@ -448,9 +577,13 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
     if (rc) return rc;
   }
   std::vector<int4> tall, shrt, simt;
-  int64_t first_row = row_lo < row_hi ? row_lo : -1;
   double exec_flops = 0, vbr_flops = 0;
-  const int64_t Npad = (N + 15) / 16 * 16;
+  const int dpc = tc ? vbr->dp / KCH : 1;
+  // short items: item order n-chunk-major keeps one 256-column B slab hot in L2 while A tiles stream
+  // (RB_SHORT_ORDER=g switches to block-row-major)
+  const char* order_env = std::getenv("RB_SHORT_ORDER");
+  const bool short_g_major = order_env && order_env[0] == 'g';
+  std::vector<int32_t> short_rows;
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
@@ -463,22 +596,29 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
         vbr_flops += 2.0 * nb * std::min(SIMT_ROWS, h - r0) * (double)vbr->dp * N;
       }
     } else if (is_short_row(h)) {
-      for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS) shrt.push_back(make_int4((int)g, hp_of(h), (int)n0, nb));
-      exec_flops += 2.0 * nb * hp_of(h) * vbr->dp * ((N + 127) / 128 * 128);
+      short_rows.push_back((int32_t)g);
+      exec_flops += 2.0 * nb * dpc * KCH * hp_of(h) * (double)((N + 127) / 128 * 128);
       vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
     } else {
-      for (int m = 0; m < (h + TALL_BM - 1) / TALL_BM; ++m) {
-        if (rp[g] + m * TALL_BM < row_lo || rp[g] + m * TALL_BM >= row_hi) continue;
+      for (int m = 0; m < (h + PAIR_BM - 1) / PAIR_BM; ++m) {
+        if (rp[g] + m * PAIR_BM < row_lo || rp[g] + m * PAIR_BM >= row_hi) continue;
         for (int64_t n0 = 0; n0 < N; n0 += TALL_BN) tall.push_back(make_int4((int)g, m, (int)n0, nb));
-        exec_flops += 2.0 * nb * TALL_BM * vbr->dp * Npad;
-        vbr_flops += 2.0 * nb * std::min(TALL_BM, h - m * TALL_BM) * (double)vbr->dp * N;
+        exec_flops += 2.0 * nb * dpc * KCH * PAIR_BM * (double)((N + TALL_BN - 1) / TALL_BN * TALL_BN);
+        vbr_flops += 2.0 * nb * std::min(PAIR_BM, h - m * PAIR_BM) * (double)vbr->dp * N;
       }
     }
   }
-  // Longest-first order for the tensor-core kernels (LPT against the tail), stable.
-  auto by_work = [](const int4& x, const int4& y) { return x.w > y.w; };
-  std::stable_sort(tall.begin(), tall.end(), by_work);
-  std::stable_sort(shrt.begin(), shrt.end(), by_work);
+  if (short_g_major) {
+    for (int32_t g : short_rows)
+      for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS)
+        shrt.push_back(make_int4(g, hp_of(rp[g + 1] - rp[g]), (int)n0, bp[g + 1] - bp[g]));
+  } else {
+    for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS)
+      for (int32_t g : short_rows) shrt.push_back(make_int4(g, hp_of(rp[g + 1] - rp[g]), (int)n0, bp[g + 1] - bp[g]));
+  }
+  // Longest-first (LPT against the tail) for the tall items, stable so the N chunks of one pair tile
+  // stay adjacent (they run concurrently and share the A tile through L2).
+  std::stable_sort(tall.begin(), tall.end(), [](const int4& x, const int4& y) { return x.w > y.w; });
 
   auto* p = new rb_spmm_plan();
   p->v = *vbr;
@@ -528,7 +668,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   p->info.n_items_simt = p->n_simt;
   p->info.executed_flops = exec_flops;
   p->info.vbr_flops = vbr_flops;
-  p->info.row_begin_perm = first_row;
+  p->info.row_begin_perm = row_lo < row_hi ? row_lo : -1;
   *out = p;
   return RB_OK;
 }
@@ -564,6 +704,7 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.ldc = ldc;
   a.N = (int32_t)p->N;
   a.ab_fmt = p->b_dtype == RB_BF16 ? 1u : 0u;
+  a.a_evict_first = 0;
   if (p->b_dtype == RB_F32) {
     if (p->n_simt > 0) {
       a.items = p->d_items;
@@ -577,8 +718,8 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   }
   static bool attr_done = false;
   if (!attr_done) {
-    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
-    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
+    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
+    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
     attr_done = true;
   }
   CUtensorMap tmB;
@@ -589,25 +730,24 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
     int rc = make_tmap_2d(&tmB, B, dt, (uint64_t)p->N, (uint64_t)p->v.n_cols, (uint64_t)ldb * 2, 64, 64);
     if (rc) return rc;
   }
+  int dev = 0, sms = kNumSMs;
+  RB_CUDA_TRY(cudaGetDevice(&dev));
+  RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (p->n_tall > 0) {
     a.items = p->d_items;
     a.n_items = (int32_t)p->n_tall;
-    spmm_tall_kernel<<<(unsigned)p->n_tall, 128, SMEM_TC, stream>>>(p->tmA128, tmB, a);
+    const int pairs = (int)std::min<int64_t>(sms / 2, p->n_tall);
+    spmm_tall2_kernel<<<(unsigned)(2 * pairs), TC_THREADS, SMEM_TALL, stream>>>(p->tmA128, tmB, a);
     RB_CUDA_TRY(cudaGetLastError());
   }
   if (p->n_short > 0) {
     a.items = p->d_items + p->n_tall;
     a.n_items = (int32_t)p->n_short;
-    spmm_short_kernel<<<(unsigned)p->n_short, 128, SMEM_TC, stream>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
-                                                                        tmB, a);
+    a.a_evict_first = 1;
+    const int ctas = (int)std::min<int64_t>(sms, p->n_short);
+    spmm_short2_kernel<<<(unsigned)ctas, TC_THREADS, SMEM_SHORT, stream>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
+                                                                          tmB, a);
     RB_CUDA_TRY(cudaGetLastError());
   }
   return RB_OK;
-}
-
-extern "C" int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* blk_ptr, int64_t n_block_rows,
-                                   int32_t b_dtype, int32_t dp, int32_t shard, int32_t n_shards, int64_t* row_begin,
-                                   int64_t* row_end) {
-  if (!row_partition || !blk_ptr || !row_begin || !row_end || n_block_rows < 0) return fail(RB_EINVAL, "bad arguments");
-  return shard_range(row_partition, blk_ptr, n_block_rows, b_dtype, dp, shard, n_shards, row_begin, row_end);
 }

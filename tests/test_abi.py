@@ -54,11 +54,11 @@ def test_shard_ranges_partition_permuted_rows(name, precision, world):
     assert ranges[0][0] == 0 and ranges[-1][1] == n
     for (b0, e0), (b1, e1) in zip(ranges, ranges[1:]):
         assert e0 == b1 and b0 <= e0
-    # cuts fall on work-unit boundaries: block-row starts, or 128-row M-tile starts of tall rows
+    # cuts fall on work-unit boundaries: block-row starts, or 256-row pair-tile starts of tall rows
     starts = set(rp.tolist())
     for g in range(len(rp) - 1):
         h = rp[g + 1] - rp[g]
-        step = 8 if precision == "fp32" else (h if h <= 128 else 128)
+        step = 8 if precision == "fp32" else (h if h <= 128 else 256)
         starts.update(range(int(rp[g]), int(rp[g + 1]), int(step)))
     for b, e in ranges:
         assert b in starts or b == n
