@@ -70,6 +70,7 @@ struct SpmmArgs {
   int32_t N;
   uint32_t ab_fmt;      // 0 = f16, 1 = bf16
   uint32_t a_evict_first;  // L2 policy of A-tile loads: 1 = evict_first, 0 = evict_normal
+  int32_t short_ns;        // C columns per short item: 128 or 256
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int b_begin = a.blk_ptr[g];
         const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
         const int64_t row0 = a.grp_tile_row[g];
-        const int n_boxes = min(4, (a.N - n0 + 63) / 64);
+        const int n_boxes = min(a.short_ns / 64, (a.N - n0 + 63) / 64);
         const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
         for (int k = 0; k < nk; ++k) {
           mbar_wait(&empty[ps.s], ps.ph ^ 1);
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int g = it.x, hp = it.y, n0 = it.z;
         const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
         if (nk == 0) continue;
-        const int n_mt = min(2, (a.N - n0 + 127) / 128);
+        const int n_mt = min(a.short_ns / 128, (a.N - n0 + 127) / 128);
         const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int p0 = a.row_partition[g];
       const int h = a.row_partition[g + 1] - p0;
       const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
-      const int n_mt = min(2, (a.N - n0 + 127) / 128);
+      const int n_mt = min(a.short_ns / 128, (a.N - n0 + 127) / 128);
       if (nk > 0) {
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
@@ -439,10 +440,18 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, co
     const int k0 = a.col_bounds[s], w = a.col_bounds[s + 1] - k0;
     const float* t = tiles + (base + (int64_t)(b - b0) * hp + r0) * dp;
     const float* bp = B + (int64_t)k0 * ldb + n;
-    for (int k = 0; k < w; ++k) {
-      const float bv = nv ? __ldg(bp + (int64_t)k * ldb) : 0.f;
+    if (rows == 1) {  // most short block rows have h = 1 (config 1): no wasted FMAs on padding rows
+      for (int k = 0; k < w; ++k) {
+        const float bv = nv ? __ldg(bp + (int64_t)k * ldb) : 0.f;
+        acc[0] = __fmaf_rn(__ldg(t + k), bv, acc[0]);
+      }
+    } else {
+      for (int k = 0; k < w; ++k) {
+        const float bv = nv ? __ldg(bp + (int64_t)k * ldb) : 0.f;
 #pragma unroll
-      for (int r = 0; r < SIMT_ROWS; ++r) acc[r] = __fmaf_rn(__ldg(t + r * dp + k), bv, acc[r]);
+        for (int r = 0; r < SIMT_ROWS; ++r)
+          if (r < rows) acc[r] = __fmaf_rn(__ldg(t + r * dp + k), bv, acc[r]);
+      }
     }
   }
   if (nv) {
@@ -538,6 +547,7 @@ struct rb_spmm_plan {
   int64_t N;
   int32_t b_dtype;
   int4* d_items = nullptr;  // tall items, then short items, then simt items
+  int32_t short_ns = rb::SHORT_NS;
   int64_t n_tall = 0, n_short = 0, n_simt = 0;
   CUtensorMap tmA16, tmA32, tmA64, tmA128;
   rb_spmm_info info;
@@ -583,6 +593,11 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   // (RB_SHORT_ORDER=g switches to block-row-major)
   const char* order_env = std::getenv("RB_SHORT_ORDER");
   const bool short_g_major = order_env && order_env[0] == 'g';
+  // column chunk of the short items: 256 (two M-tiles; each A tile is read N/256 times).  Measured on
+  // config 5 (B slab per chunk 134 MB > L2): 128 halves B misses but doubles A reads and is 1.5x
+  // slower, so 256 is the default.  RB_SHORT_NS=128 overrides.
+  int32_t short_ns = rb::SHORT_NS;
+  if (const char* ns_env = std::getenv("RB_SHORT_NS")) short_ns = std::atoi(ns_env) >= 256 ? 256 : 128;
   std::vector<int32_t> short_rows;
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
@@ -597,7 +612,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       }
     } else if (is_short_row(h)) {
       short_rows.push_back((int32_t)g);
-      exec_flops += 2.0 * nb * dpc * KCH * hp_of(h) * (double)((N + 127) / 128 * 128);
+      exec_flops += 2.0 * nb * dpc * KCH * hp_of(h) * (double)((N + 127) / 128 * 128);  // M tiles of 128
       vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
     } else {
       for (int m = 0; m < (h + PAIR_BM - 1) / PAIR_BM; ++m) {
@@ -610,10 +625,10 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   }
   if (short_g_major) {
     for (int32_t g : short_rows)
-      for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS)
+      for (int64_t n0 = 0; n0 < N; n0 += short_ns)
         shrt.push_back(make_int4(g, hp_of(rp[g + 1] - rp[g]), (int)n0, bp[g + 1] - bp[g]));
   } else {
-    for (int64_t n0 = 0; n0 < N; n0 += SHORT_NS)
+    for (int64_t n0 = 0; n0 < N; n0 += short_ns)
       for (int32_t g : short_rows) shrt.push_back(make_int4(g, hp_of(rp[g + 1] - rp[g]), (int)n0, bp[g + 1] - bp[g]));
   }
   // Longest-first (LPT against the tail) for the tall items, stable so the N chunks of one pair tile
@@ -624,6 +639,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   p->v = *vbr;
   p->N = N;
   p->b_dtype = b_dtype;
+  p->short_ns = short_ns;
   p->n_tall = (int64_t)tall.size();
   p->n_short = (int64_t)shrt.size();
   p->n_simt = (int64_t)simt.size();
@@ -705,6 +721,7 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.N = (int32_t)p->N;
   a.ab_fmt = p->b_dtype == RB_BF16 ? 1u : 0u;
   a.a_evict_first = 0;
+  a.short_ns = p->short_ns;
   if (p->b_dtype == RB_F32) {
     if (p->n_simt > 0) {
       a.items = p->d_items;

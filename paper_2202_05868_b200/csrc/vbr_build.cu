@@ -23,6 +23,7 @@ struct VbrWs {
   int32_t* group_of_row;  // [n]
   int32_t* pos_of_row;    // [n]
   unsigned long long* gbits;  // [H*W]
+  unsigned long long* rbits;  // [n*W] per-row segment bits
   int32_t* wprefix;       // [H*W]
   int32_t* blk_cnt;       // [H+1]
   int64_t* tile_cnt;      // [H+1]
@@ -51,6 +52,7 @@ VbrWs carve(void* base, int64_t n, int64_t H, int64_t W, int64_t n_seg) {
   w.group_of_row = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(n, 1));
   w.pos_of_row = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(n, 1));
   w.gbits = (unsigned long long*)take(sizeof(uint64_t) * std::max<int64_t>(H * W, 1));
+  w.rbits = (unsigned long long*)take(sizeof(uint64_t) * std::max<int64_t>(n * W, 1));
   w.wprefix = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(H * W, 1));
   w.blk_cnt = (int32_t*)take(sizeof(int32_t) * (H + 1));
   w.tile_cnt = (int64_t*)take(sizeof(int64_t) * (H + 1));
@@ -97,20 +99,50 @@ __global__ void rpart_kernel(const int64_t* __restrict__ row_partition, int64_t 
   }
 }
 
-// warp per row: OR the row's segments into its block row's bitset (vbr.py:108-112)
-__global__ void group_bits_kernel(const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col_idx, int64_t n,
-                                  SegMap seg, const int32_t* __restrict__ group_of_row, int64_t W,
-                                  unsigned long long* gbits) {
+// Stored block columns of a block row (vbr.py:108-112) = OR of its rows' segment bitsets.
+// Pass 1 (row_bits_kernel): warp per row, segment bits of that row (atomics only within the row).
+// Pass 2 (group_or_kernel): warp per chunk of 256 permuted positions; lane w ORs word w of the
+// chunk's rows in registers and flushes one atomicOr per (block row, word) it touched, so a single
+// huge block row (config 2: 32768 rows in one group) does not serialise on 8 words.
+__global__ void row_bits_kernel(const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col_idx, int64_t n,
+                                SegMap seg, int64_t W, unsigned long long* rbits) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
     const int64_t s0 = row_ptr[r], s1 = row_ptr[r + 1];
-    if (s1 == s0) continue;
-    unsigned long long* gb = gbits + (int64_t)group_of_row[r] * W;
+    unsigned long long* rb = rbits + r * W;
     for (int64_t j = s0 + lane; j < s1; j += 32) {
       const int32_t s = seg((int32_t)col_idx[j]);
-      // columns are strictly increasing, so segments are non-decreasing: OR once per segment run
-      if (j == s0 || seg((int32_t)col_idx[j - 1]) != s) atomicOr(gb + (s >> 6), 1ull << (s & 63));
+      // columns strictly increase, so segments are non-decreasing: OR once per segment run
+      if (j == s0 || seg((int32_t)col_idx[j - 1]) != s) atomicOr(rb + (s >> 6), 1ull << (s & 63));
+    }
+  }
+}
+
+constexpr int kOrChunk = 256;
+__global__ void group_or_kernel(const unsigned long long* __restrict__ rbits, const int32_t* __restrict__ perm32,
+                                const int32_t* __restrict__ group_of_row, int64_t n, int64_t W,
+                                unsigned long long* gbits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_chunks = (n + kOrChunk - 1) / kOrChunk;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < n_chunks; c += warps) {
+    const int64_t p0 = c * kOrChunk, p1 = min(n, p0 + kOrChunk);
+    for (int64_t w0 = 0; w0 < W; w0 += 32) {
+      const int64_t w = w0 + lane;
+      unsigned long long acc = 0;
+      int32_t g_cur = group_of_row[perm32[p0]];
+      for (int64_t p = p0; p < p1; ++p) {
+        const int32_t r = perm32[p];
+        const int32_t g = group_of_row[r];
+        if (g != g_cur) {
+          if (w < W && acc) atomicOr(gbits + (int64_t)g_cur * W + w, acc);
+          acc = 0;
+          g_cur = g;
+        }
+        if (w < W) acc |= rbits[(int64_t)r * W + w];
+      }
+      if (w < W && acc) atomicOr(gbits + (int64_t)g_cur * W + w, acc);
     }
   }
 }
@@ -239,8 +271,10 @@ extern "C" int rb_vbr_plan(int64_t n_rows, int64_t n_cols, const int64_t* row_pt
   if (n_rows > 0) {
     positions_kernel<<<grid_for(n_rows, 256), 256, 0, stream>>>(row_perm, row_partition, n_rows, H, ws.group_of_row,
                                                                 ws.pos_of_row, perm32, ws.err);
-    group_bits_kernel<<<grid_for(n_rows, 8), 256, 0, stream>>>(row_ptr, col_idx, n_rows, seg, ws.group_of_row, W,
-                                                               ws.gbits);
+    RB_CUDA_TRY(cudaMemsetAsync(ws.rbits, 0, sizeof(uint64_t) * n_rows * W, stream));
+    row_bits_kernel<<<grid_for(n_rows, 8), 256, 0, stream>>>(row_ptr, col_idx, n_rows, seg, W, ws.rbits);
+    group_or_kernel<<<grid_for((n_rows + kOrChunk - 1) / kOrChunk, 8), 256, 0, stream>>>(
+        ws.rbits, perm32, ws.group_of_row, n_rows, W, ws.gbits);
   }
   if (H > 0)
     count_kernel<<<grid_for(H, 8), 256, 0, stream>>>(ws.gbits, H, W, row_partition, ws.wprefix, ws.blk_cnt,
