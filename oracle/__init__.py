@@ -51,6 +51,8 @@ def _load():
         lib.orc_block_1sa.argtypes = [I, P, P, P, I, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, P]
         lib.orc_vbr_blocks.argtypes = [I, P, P, P, I, P, P, I, P, P]
+        lib.orc_block_1sa_pruned.argtypes = [I, P, P, P, I, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, P, P]
         _lib = lib
     return _lib
 
@@ -76,7 +78,7 @@ def quotient(row_ptr, col_idx, boundaries):
 
 
 def block_1sa_arrays(row_ptr, col_idx, boundaries, tau=0.5, similarity="jaccard", bounded=True,
-                     pattern_update=True, use_compression=True) -> dict:
+                     pattern_update=True, use_compression=True, pruned=False) -> dict:
     """Array form of block_1sa (blocking.py:283-306).
 
     Returns dict(group_of, row_perm, group_ptr, seed_size, pattern_ptr, pattern_idx, n_groups).
@@ -91,11 +93,16 @@ def block_1sa_arrays(row_ptr, col_idx, boundaries, tau=0.5, similarity="jaccard"
         pattern_ptr=np.zeros(n + 1, np.int64), pattern_idx=np.zeros(max(nnz, 1), np.int64),
     )
     H = np.zeros(1, np.int64)
-    rc = _load().orc_block_1sa(n, _ptr(row_ptr), _ptr(col_idx), _ptr(b), n_seg, float(tau),
-                               int(similarity == "cosine"), int(bool(bounded)), int(bool(pattern_update)),
-                               int(bool(use_compression)), _ptr(out["group_of"]), _ptr(out["row_perm"]),
-                               _ptr(out["group_ptr"]), _ptr(out["seed_size"]), _ptr(out["pattern_ptr"]),
-                               _ptr(out["pattern_idx"]), _ptr(H))
+    args = (n, _ptr(row_ptr), _ptr(col_idx), _ptr(b), n_seg, float(tau), int(similarity == "cosine"),
+            int(bool(bounded)), int(bool(pattern_update)), int(bool(use_compression)), _ptr(out["group_of"]),
+            _ptr(out["row_perm"]), _ptr(out["group_ptr"]), _ptr(out["seed_size"]), _ptr(out["pattern_ptr"]),
+            _ptr(out["pattern_idx"]), _ptr(H))
+    if pruned:
+        stats = np.zeros(3, np.int64)
+        rc = _load().orc_block_1sa_pruned(*args, _ptr(stats))
+        out["stats"] = dict(rounds=int(stats[0]), postings_visited=int(stats[1]), candidates=int(stats[2]))
+    else:
+        rc = _load().orc_block_1sa(*args)
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     h = int(H[0])

@@ -233,3 +233,212 @@ int orc_vbr_blocks(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_id
   free(acc);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Pruned restatement of the same greedy scan (SURVEY App. A "exact pruning"), used as the oracle at
+ * sizes where the dense O(m^2 W) scan is infeasible (config 3, R-MAT 2^20).  Identical output to
+ * orc_block_1sa; candidates of a round are enumerated from an inverted index over a PREFIX of the
+ * current pattern (its psize - t + 1 rarest segments, t = the least intersection any acceptable
+ * candidate must have), which is exact because every acceptable candidate shares >= t segments
+ * with P.  Falls back to the full scan when t == 0 (tau == 0 or an empty pattern).
+ * Work counters: stats[0] rounds, stats[1] postings entries visited, stats[2] candidates evaluated. */
+static int cmp_i64(const void* a, const void* b) {
+  int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+int orc_block_1sa_pruned(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx, const int64_t* bounds,
+                         int64_t n_seg, double tau, int cosine, int bounded, int pattern_update, int use_compression,
+                         int64_t* group_of, int64_t* row_perm, int64_t* group_ptr, int64_t* seed_size,
+                         int64_t* pattern_ptr, int64_t* pattern_idx, int64_t* n_groups_out, int64_t* stats) {
+  /* per-row sorted unique segment lists */
+  int64_t* rs_ptr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+  int64_t nnz = row_ptr[n_rows];
+  int64_t* rs = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nnz + 1));
+  if (!rs_ptr || !rs) return -1;
+  rs_ptr[0] = 0;
+  for (int64_t i = 0; i < n_rows; ++i) {
+    int64_t k = rs_ptr[i], last = -1;
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      int64_t s = seg_of(bounds, n_seg, col_idx[p]);
+      if (s != last) { rs[k++] = s; last = s; }
+    }
+    rs_ptr[i + 1] = k;
+  }
+  /* compression keyed on the exact segment list (first-occurrence order) */
+  int64_t* item_of_row = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+  int64_t* reps = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_rows + 1));
+  int64_t m = 0;
+  if (use_compression) {
+    int64_t cap = 16;
+    while (cap < 2 * n_rows) cap <<= 1;
+    int64_t* table = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+    for (int64_t t = 0; t < cap; ++t) table[t] = -1;
+    for (int64_t i = 0; i < n_rows; ++i) {
+      uint64_t h = 1469598103934665603ull ^ (uint64_t)(rs_ptr[i + 1] - rs_ptr[i]);
+      for (int64_t p = rs_ptr[i]; p < rs_ptr[i + 1]; ++p) { h ^= (uint64_t)rs[p]; h *= 1099511628211ull; h ^= h >> 29; }
+      int64_t t = (int64_t)(h & (uint64_t)(cap - 1));
+      for (;;) {
+        int64_t it = table[t];
+        if (it < 0) { table[t] = m; reps[m] = i; item_of_row[i] = m; ++m; break; }
+        int64_t r = reps[it];
+        int64_t len = rs_ptr[i + 1] - rs_ptr[i];
+        if (rs_ptr[r + 1] - rs_ptr[r] == len && memcmp(rs + rs_ptr[r], rs + rs_ptr[i], sizeof(int64_t) * (size_t)len) == 0) {
+          item_of_row[i] = it;
+          break;
+        }
+        t = (t + 1) & (cap - 1);
+      }
+    }
+    free(table);
+  } else {
+    for (int64_t i = 0; i < n_rows; ++i) { reps[i] = i; item_of_row[i] = i; }
+    m = n_rows;
+  }
+  /* item segment lists and inverted index (postings ascending by item) */
+  int64_t* isz = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  int64_t* post_ptr = (int64_t*)calloc((size_t)(n_seg + 2), sizeof(int64_t));
+  for (int64_t j = 0; j < m; ++j) {
+    int64_t r = reps[j];
+    isz[j] = rs_ptr[r + 1] - rs_ptr[r];
+    for (int64_t p = rs_ptr[r]; p < rs_ptr[r + 1]; ++p) post_ptr[rs[p] + 1]++;
+  }
+  for (int64_t s = 0; s < n_seg; ++s) post_ptr[s + 1] += post_ptr[s];
+  int64_t* post = (int64_t*)malloc(sizeof(int64_t) * (size_t)(post_ptr[n_seg] + 1));
+  int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_seg + 1));
+  memcpy(fill, post_ptr, sizeof(int64_t) * (size_t)(n_seg + 1));
+  for (int64_t j = 0; j < m; ++j) {
+    int64_t r = reps[j];
+    for (int64_t p = rs_ptr[r]; p < rs_ptr[r + 1]; ++p) post[fill[rs[p]]++] = j;
+  }
+  int64_t W = n_words_of(n_seg);
+  uint64_t* P = (uint64_t*)calloc((size_t)W, sizeof(uint64_t));
+  int64_t* plist = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_seg + 1));
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(2 * n_seg + 2));
+  int64_t* group_of_item = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  int64_t* seed_item = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  int64_t* stamp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  uint8_t* okv = (uint8_t*)malloc((size_t)(m + 1));
+  int64_t* cand = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  /* empty items (pattern size 0), ascending: the only candidates of an empty pattern when tau > 0 */
+  int64_t* empt = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  int64_t n_empty = 0;
+  for (int64_t j = 0; j < m; ++j) { group_of_item[j] = -1; stamp[j] = -1; if (isz[j] == 0) empt[n_empty++] = j; }
+  int64_t H = 0, next = 0, round = 0;
+  stats[0] = stats[1] = stats[2] = 0;
+  while (next < m) {
+    int64_t seed = next;
+    group_of_item[seed] = H;
+    seed_item[H] = seed;
+    int64_t r0 = reps[seed];
+    memset(P, 0, sizeof(uint64_t) * (size_t)W);
+    int64_t psize = 0;
+    for (int64_t p = rs_ptr[r0]; p < rs_ptr[r0 + 1]; ++p) { P[rs[p] >> 6] |= 1ull << (rs[p] & 63); plist[psize++] = rs[p]; }
+    double capv = bounded ? (double)psize / (1.0 - 0.5 * tau) : 0.0;
+    int64_t pos = seed + 1;
+    for (;;) {
+      ++round;
+      ++stats[0];
+      /* least intersection t of any acceptable candidate (conservative, exact) */
+      int64_t t;
+      if (!cosine) { double lb = tau * (double)psize; t = (int64_t)ceil(lb); }
+      else { double lb = tau * tau * (double)psize * (1.0 - 1e-12); t = (int64_t)ceil(lb); if (t < 0) t = 0; }
+      int64_t nc = 0;
+      if (t >= 1 && psize > 0) {
+        /* prefix = the psize - t + 1 segments of P with the shortest postings lists */
+        int64_t npre = psize - t + 1;
+        for (int64_t q = 0; q < psize; ++q) { order[2 * q] = post_ptr[plist[q] + 1] - post_ptr[plist[q]]; order[2 * q + 1] = plist[q]; }
+        /* partial selection sort is fine for small psize; qsort pairs otherwise */
+        for (int64_t a = 0; a < npre; ++a) {
+          int64_t best = a;
+          for (int64_t b = a + 1; b < psize; ++b)
+            if (order[2 * b] < order[2 * best] || (order[2 * b] == order[2 * best] && order[2 * b + 1] < order[2 * best + 1])) best = b;
+          int64_t x0 = order[2 * a], x1 = order[2 * a + 1];
+          order[2 * a] = order[2 * best]; order[2 * a + 1] = order[2 * best + 1];
+          order[2 * best] = x0; order[2 * best + 1] = x1;
+        }
+        for (int64_t a = 0; a < npre; ++a) {
+          int64_t s = order[2 * a + 1];
+          int64_t lo = post_ptr[s], hi = post_ptr[s + 1];
+          while (lo < hi) { int64_t mid = (lo + hi) / 2; if (post[mid] < pos) lo = mid + 1; else hi = mid; }
+          for (int64_t q = lo; q < post_ptr[s + 1]; ++q) {
+            ++stats[1];
+            int64_t j = post[q];
+            if (group_of_item[j] >= 0 || stamp[j] == round) continue;
+            stamp[j] = round;
+            cand[nc++] = j;
+          }
+        }
+      } else if (psize == 0 && tau > 0.0) {
+        for (int64_t q = 0; q < n_empty; ++q) if (empt[q] >= pos && group_of_item[empt[q]] < 0) cand[nc++] = empt[q];
+      } else {
+        for (int64_t j = pos; j < m; ++j) if (group_of_item[j] < 0) cand[nc++] = j;
+      }
+      /* evaluate candidates; first growing hit */
+      int64_t jstar = m;
+      for (int64_t q = 0; q < nc; ++q) {
+        int64_t j = cand[q], rj = reps[j], inter = 0;
+        ++stats[2];
+        for (int64_t p = rs_ptr[rj]; p < rs_ptr[rj + 1]; ++p) inter += (P[rs[p] >> 6] >> (rs[p] & 63)) & 1;
+        int ok = accept(inter, psize, isz[j], tau, cosine, bounded, capv);
+        okv[j] = (uint8_t)ok;
+        if (ok && pattern_update && inter < isz[j] && j < jstar) jstar = j;
+      }
+      for (int64_t q = 0; q < nc; ++q) {
+        int64_t j = cand[q];
+        if (okv[j] && j < jstar) group_of_item[j] = H;
+      }
+      if (jstar < m) {
+        int64_t rj = reps[jstar];
+        group_of_item[jstar] = H;
+        for (int64_t p = rs_ptr[rj]; p < rs_ptr[rj + 1]; ++p) {
+          int64_t s = rs[p];
+          if (!((P[s >> 6] >> (s & 63)) & 1)) { P[s >> 6] |= 1ull << (s & 63); plist[psize++] = s; }
+        }
+        pos = jstar + 1;
+        continue;
+      }
+      break;
+    }
+    ++H;
+    while (next < m && group_of_item[next] >= 0) ++next;
+  }
+  /* assembly identical to orc_block_1sa */
+  int64_t* icnt = (int64_t*)calloc((size_t)(m + 1), sizeof(int64_t));
+  int64_t* cnt = (int64_t*)calloc((size_t)(H + 1), sizeof(int64_t));
+  int64_t* iptr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  int64_t* gcur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(H + 1));
+  for (int64_t r = 0; r < n_rows; ++r) icnt[item_of_row[r]]++;
+  for (int64_t j = 0; j < m; ++j) cnt[group_of_item[j]] += icnt[j];
+  group_ptr[0] = 0;
+  for (int64_t g = 0; g < H; ++g) group_ptr[g + 1] = group_ptr[g] + cnt[g];
+  for (int64_t g = 0; g < H; ++g) gcur[g] = group_ptr[g];
+  for (int64_t j = 0; j < m; ++j) { iptr[j] = gcur[group_of_item[j]]; gcur[group_of_item[j]] += icnt[j]; }
+  for (int64_t r = 0; r < n_rows; ++r) { int64_t it = item_of_row[r]; row_perm[iptr[it]++] = r; group_of[r] = group_of_item[it]; }
+  /* patterns: sorted union of member segment lists */
+  int64_t* mark = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_seg + 1));
+  for (int64_t s = 0; s < n_seg; ++s) mark[s] = -1;
+  int64_t* mem_ptr = (int64_t*)calloc((size_t)(H + 1), sizeof(int64_t));
+  int64_t* mem = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + 1));
+  for (int64_t j = 0; j < m; ++j) mem_ptr[group_of_item[j] + 1]++;
+  for (int64_t g = 0; g < H; ++g) mem_ptr[g + 1] += mem_ptr[g];
+  for (int64_t g = 0; g < H; ++g) gcur[g] = mem_ptr[g];
+  for (int64_t j = 0; j < m; ++j) mem[gcur[group_of_item[j]]++] = j;
+  pattern_ptr[0] = 0;
+  for (int64_t g = 0; g < H; ++g) {
+    int64_t k = pattern_ptr[g];
+    for (int64_t q = mem_ptr[g]; q < mem_ptr[g + 1]; ++q) {
+      int64_t r = reps[mem[q]];
+      for (int64_t p = rs_ptr[r]; p < rs_ptr[r + 1]; ++p)
+        if (mark[rs[p]] != g) { mark[rs[p]] = g; pattern_idx[k++] = rs[p]; }
+    }
+    qsort(pattern_idx + pattern_ptr[g], (size_t)(k - pattern_ptr[g]), sizeof(int64_t), cmp_i64);
+    pattern_ptr[g + 1] = k;
+    seed_size[g] = isz[seed_item[g]];
+  }
+  *n_groups_out = H;
+  free(mark); free(mem_ptr); free(mem); free(icnt); free(cnt); free(iptr); free(gcur);
+  free(P); free(plist); free(order); free(group_of_item); free(seed_item); free(stamp); free(okv); free(cand); free(empt);
+  free(isz); free(post_ptr); free(post); free(fill); free(rs_ptr); free(rs); free(item_of_row); free(reps);
+  return 0;
+}

@@ -15,8 +15,11 @@
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -488,6 +491,771 @@ __global__ void pattern_kernel(const unsigned long long* __restrict__ gbits, int
   }
 }
 
+
+// =============================================================================================
+// Sparse pipeline (large W, e.g. config 3: 32768 segments): segment LISTS instead of bitsets and an
+// inverted index (segment -> items ascending).  The greedy kernel enumerates, per round, only the
+// candidates that share a segment with a PREFIX of the current pattern: every acceptable candidate
+// shares >= t = ceil(fl(tau*psize)) segments with P (jaccard; cosine: tau^2*psize, conservative),
+// so it must hit any psize - t + 1 of P's segments (exact).  The prefix is every
+// segment whose postings length falls in the log2-length buckets that first reach psize - t + 1
+// segments (a superset of the rarest ones, hence still exact).  t == 0 (tau == 0) scans all
+// unassigned items; an empty pattern (tau > 0) only the empty items.
+
+constexpr int64_t kDenseMaxWords = 64;
+
+bool use_sparse_path(int64_t W) {
+  const char* m = std::getenv("RB_1SA_MODE");
+  if (m && m[0] == 's') return true;
+  if (m && m[0] == 'd') return false;
+  return W > kDenseMaxWords;
+}
+
+struct SWs {
+  int32_t* sizes;          // [n]
+  int64_t* rs_ptr;         // [n+1]
+  int32_t* rs;             // [nnz]   row segment lists
+  unsigned long long* keys_a;  // [max(n, nnz)]
+  unsigned long long* keys_b;  // [max(n, nnz)]
+  int32_t* vals_a;         // [n]
+  int32_t* vals_b;         // [n]
+  int32_t* t0;             // [n+1]
+  int32_t* t1;             // [n+1]
+  int32_t* item_of_row;    // [n]
+  int32_t* reps;           // [n]
+  int32_t* item_size;      // [n]
+  int64_t* item_ptr;       // [n+1]
+  int32_t* item_seg;       // [nnz]
+  int64_t* post_ptr;       // [n_seg+1]
+  int32_t* post_item;      // [nnz]
+  int32_t* seg_cnt;        // [n_seg+1]
+  int32_t* empties;        // [n]
+  int32_t* n_empty;        // [1]
+  int32_t* group_of_item;  // [n]
+  int32_t* stamp;          // [n]
+  int32_t* cand_j;         // [3*n]
+  uint8_t* cand_ok;        // [3*n]
+  int32_t* seed_item;      // [n]
+  int32_t* ctrl;           // [32]
+  int32_t* scratch;        // [blocks * 3 * (n_seg+1)]
+  int64_t* pcnt;           // [n+1]
+  int32_t* b32;            // [n_seg+1]
+  void* cub_tmp;
+  size_t cub_bytes;
+  size_t total;
+};
+
+constexpr int kSparseBlocks = 148;
+constexpr int kSparseThreads = 512;
+
+size_t sparse_cub_bytes(int64_t n, int64_t nnz, int64_t n_seg) {
+  const int nn = (int)std::max<int64_t>(n + 1, 2), ee = (int)std::max<int64_t>(nnz + 1, 2);
+  size_t a = 0, b = 0, c = 0, d = 0, e = 0, f = 0, g = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (int32_t*)nullptr, (int32_t*)nullptr, nn);
+  cub::DeviceRadixSort::SortKeys(nullptr, b, (unsigned long long*)nullptr, (unsigned long long*)nullptr, ee);
+  cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, nn);
+  cub::DeviceScan::ExclusiveSum(nullptr, d, (int64_t*)nullptr, (int64_t*)nullptr, std::max(nn, (int)(n_seg + 2)));
+  cub::DeviceScan::InclusiveScan(nullptr, e, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), nn);
+  cub::DeviceSelect::Unique(nullptr, f, (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int*)nullptr, ee);
+  cub::DeviceScan::ExclusiveSum(nullptr, g, (int32_t*)nullptr, (int64_t*)nullptr, std::max(nn, (int)(n_seg + 2)));
+  return std::max({a, b, c, d, e, f, g});
+}
+
+SWs carve_sparse(void* base, int64_t n, int64_t nnz, int64_t n_seg) {
+  SWs w;
+  size_t off = 0;
+  const int64_t n1 = std::max<int64_t>(n, 1), e1 = std::max<int64_t>(nnz, 1), s1 = n_seg + 1;
+  auto take = [&](size_t bytes) {
+    void* p = base ? static_cast<char*>(base) + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  w.sizes = (int32_t*)take(4 * n1);
+  w.rs_ptr = (int64_t*)take(8 * (n1 + 1));
+  w.rs = (int32_t*)take(4 * e1);
+  w.keys_a = (unsigned long long*)take(8 * std::max(n1, e1));
+  w.keys_b = (unsigned long long*)take(8 * std::max(n1, e1));
+  w.vals_a = (int32_t*)take(4 * (n1 + 1));
+  w.vals_b = (int32_t*)take(4 * (n1 + 1));
+  w.t0 = (int32_t*)take(4 * (n1 + 1));
+  w.t1 = (int32_t*)take(4 * (n1 + 1));
+  w.item_of_row = (int32_t*)take(4 * n1);
+  w.reps = (int32_t*)take(4 * n1);
+  w.item_size = (int32_t*)take(4 * (n1 + 1));
+  w.item_ptr = (int64_t*)take(8 * (n1 + 1));
+  w.item_seg = (int32_t*)take(4 * e1);
+  w.post_ptr = (int64_t*)take(8 * (s1 + 1));
+  w.post_item = (int32_t*)take(4 * e1);
+  w.seg_cnt = (int32_t*)take(4 * (s1 + 1));
+  w.empties = (int32_t*)take(4 * n1);
+  w.n_empty = (int32_t*)take(16);
+  w.group_of_item = (int32_t*)take(4 * n1);
+  w.stamp = (int32_t*)take(4 * n1);
+  w.cand_j = (int32_t*)take(4 * 3 * n1);
+  w.cand_ok = (uint8_t*)take(3 * n1);
+  w.seed_item = (int32_t*)take(4 * n1);
+  w.ctrl = (int32_t*)take(4 * 32);
+  w.scratch = (int32_t*)take(4 * (size_t)kSparseBlocks * 3 * (s1 + 1));
+  w.pcnt = (int64_t*)take(8 * (n1 + 1));
+  w.b32 = (int32_t*)take(4 * s1);
+  w.cub_bytes = sparse_cub_bytes(n, nnz, n_seg);
+  w.cub_tmp = take(w.cub_bytes);
+  w.total = off;
+  return w;
+}
+
+// warp per row: number of segment runs (= quotient pattern size, blocking.py:135)
+__global__ void seg_count_kernel(const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col_idx, int64_t n,
+                                 SegMap seg, int32_t* sizes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const int64_t s0 = row_ptr[r], s1 = row_ptr[r + 1];
+    int cnt = 0;
+    for (int64_t j = s0 + lane; j < s1; j += 32)
+      cnt += (j == s0 || seg((int32_t)col_idx[j - 1]) != seg((int32_t)col_idx[j])) ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) sizes[r] = cnt;
+  }
+}
+
+// warp per row: ascending unique segment list of the row (the quotient row, blocking.py:118-136)
+__global__ void seg_write_kernel(const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col_idx, int64_t n,
+                                 SegMap seg, const int64_t* __restrict__ rs_ptr, int32_t* rs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const int64_t s0 = row_ptr[r], s1 = row_ptr[r + 1];
+    int64_t out = rs_ptr[r];
+    for (int64_t j0 = s0; j0 < s1; j0 += 32) {
+      const int64_t j = j0 + lane;
+      int32_t sg = 0;
+      bool flag = false;
+      if (j < s1) {
+        sg = seg((int32_t)col_idx[j]);
+        flag = (j == s0) || seg((int32_t)col_idx[j - 1]) != sg;
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, flag);
+      if (flag) rs[out + __popc(b & ((1u << lane) - 1u))] = sg;
+      out += __popc(b);
+    }
+  }
+}
+
+__global__ void list_hash_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ lst, int64_t n,
+                                 unsigned long long* keys, int32_t* vals) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long h = 0x9E3779B97F4A7C15ull ^ (unsigned long long)(ptr[r + 1] - ptr[r]);
+    for (int64_t p = ptr[r]; p < ptr[r + 1]; ++p) h = mix64(h ^ (0x632BE59BD9B4E019ull * (unsigned long long)(lst[p] + 1)));
+    keys[r] = h;
+    vals[r] = (int32_t)r;
+  }
+}
+
+__device__ __forceinline__ bool lists_equal(const int64_t* ptr, const int32_t* lst, int32_t a, int32_t b) {
+  const int64_t la = ptr[a + 1] - ptr[a];
+  if (la != ptr[b + 1] - ptr[b]) return false;
+  for (int64_t k = 0; k < la; ++k)
+    if (lst[ptr[a] + k] != lst[ptr[b] + k]) return false;
+  return true;
+}
+
+__global__ void list_rep_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ lst,
+                                const int32_t* __restrict__ rows_sorted, const int32_t* __restrict__ run_start,
+                                int64_t n, int32_t* rep_of_row) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rows_sorted[p];
+    int32_t rep = r;
+    for (int64_t q = run_start[p]; q < p; ++q) {
+      const int32_t c = rows_sorted[q];
+      if (lists_equal(ptr, lst, c, r)) {
+        rep = c;
+        break;
+      }
+    }
+    rep_of_row[r] = rep;
+  }
+}
+
+__global__ void item_size_kernel(const int32_t* __restrict__ reps, const int32_t* __restrict__ sizes, int64_t m,
+                                 int32_t* item_size, int32_t* group_of_item, int32_t* stamp) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    item_size[j] = sizes[reps[j]];
+    group_of_item[j] = -1;
+    stamp[j] = -1;
+  }
+}
+
+// warp per item: copy the representative row's segment list; histogram segment frequencies
+__global__ void item_lists_kernel(const int32_t* __restrict__ reps, const int64_t* __restrict__ rs_ptr,
+                                  const int32_t* __restrict__ rs, const int64_t* __restrict__ item_ptr, int64_t m,
+                                  int32_t* item_seg, int32_t* seg_cnt, unsigned long long* pkeys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < m; j += warps) {
+    const int32_t r = reps[j];
+    const int64_t src = rs_ptr[r], len = rs_ptr[r + 1] - src, dst = item_ptr[j];
+    for (int64_t k = lane; k < len; k += 32) {
+      const int32_t s = rs[src + k];
+      item_seg[dst + k] = s;
+      atomicAdd(seg_cnt + s, 1);
+      pkeys[dst + k] = ((unsigned long long)s << 32) | (unsigned long long)(uint32_t)j;  // postings sort key
+    }
+  }
+}
+
+__global__ void postings_kernel(const unsigned long long* __restrict__ pkeys_sorted, int64_t E, int32_t* post_item) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    post_item[e] = (int32_t)(pkeys_sorted[e] & 0xffffffffull);
+}
+
+__global__ void empties_kernel(const int32_t* __restrict__ item_size, int64_t m, int32_t* empties, int32_t* n_empty) {
+  // single block: ascending list of empty items (blocking.py: an empty pattern accepts only empty rows)
+  __shared__ int32_t base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t j0 = 0; j0 < m; j0 += blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    const bool e = j < m && item_size[j] == 0;
+    const unsigned b = __ballot_sync(0xffffffffu, e);
+    __shared__ int32_t wcnt[32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) wcnt[w] = __popc(b);
+    __syncthreads();
+    int off = base;
+    for (int k = 0; k < w; ++k) off += wcnt[k];
+    if (e) empties[off + __popc(b & ((1u << lane) - 1u))] = (int32_t)j;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += wcnt[k];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_empty = base;
+}
+
+struct SGreedyArgs {
+  int32_t m, n_seg, W;
+  const int64_t* item_ptr;
+  const int32_t* item_seg;
+  const int32_t* item_size;
+  const int64_t* post_ptr;
+  const int32_t* post_item;
+  const int32_t* empties;
+  const int32_t* n_empty;
+  double tau;
+  int32_t cosine, bounded, update;
+  int32_t* group_of_item;
+  int32_t* stamp;
+  int32_t* cand_j;   // [3][m]
+  uint8_t* cand_ok;  // [3][m]
+  int32_t* seed_item;
+  int32_t* ctrl;     // [0..2] jstar slots, [3..5] candidate counts, [6] H, [8] count, [9] gen
+  int32_t* scratch;  // per block: plist | pscan | pstart, each n_seg+1
+};
+
+// block-wide exclusive scan of v over n elements stored in global scratch (in place), returns total
+__device__ int32_t block_exclusive_scan(int32_t* v, int32_t n, int32_t* smem_w /*[32]*/, int32_t* smem_carry) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) *smem_carry = 0;
+  __syncthreads();
+  for (int32_t base = 0; base < n; base += blockDim.x) {
+    const int32_t i = base + threadIdx.x;
+    const int32_t x = i < n ? v[i] : 0;
+    int32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) smem_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int32_t t = lane < nw ? smem_w[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      if (lane < nw) smem_w[lane] = t;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int32_t carry = *smem_carry;
+    const int32_t wbase = w > 0 ? smem_w[w - 1] : 0;
+    if (i < n) v[i] = carry + wbase + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 0) *smem_carry = carry + smem_w[nw - 1];
+    __syncthreads();
+  }
+  return *smem_carry;
+}
+
+__global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyArgs a) {
+  extern __shared__ unsigned long long sP[];  // pattern bits, W words
+  __shared__ int32_t s_w[32], s_carry;
+  __shared__ int32_t s_hist[33];
+  __shared__ int32_t s_js, s_bstar, s_T, s_next, s_inter;
+  __shared__ int32_t s_psize, s_pos, s_seed, s_g, s_rid, s_acc_list, s_acc_cnt, s_acc_limit, s_acc_g, s_pending_seed;
+  __shared__ double s_cap;
+
+  const int32_t m = a.m;
+  const double tau = a.tau;
+  const double cap_den = __dsub_rn(1.0, __dmul_rn(0.5, tau));
+  int32_t* plist = a.scratch + (size_t)blockIdx.x * 3 * (a.n_seg + 1);
+  int32_t* pscan = plist + (a.n_seg + 1);
+  int32_t* pstart = pscan + (a.n_seg + 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+
+  for (int w = threadIdx.x; w < a.W; w += blockDim.x) sP[w] = 0ull;
+  __syncthreads();
+  // seed item 0
+  {
+    const int64_t p0 = a.item_ptr[0], len = a.item_ptr[1] - p0;
+    for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
+      const int32_t sg = a.item_seg[p0 + k];
+      plist[k] = sg;
+      atomicOr(&sP[sg >> 6], 1ull << (sg & 63));
+    }
+    if (threadIdx.x == 0) {
+      s_psize = (int32_t)len;
+      s_cap = __ddiv_rn((double)len, cap_den);
+      s_pos = 1;
+      s_seed = 0;
+      s_g = 0;
+      s_rid = 0;
+      s_acc_cnt = 0;
+      s_pending_seed = -1;
+      if (blockIdx.x == 0) {
+        a.group_of_item[0] = 0;
+        a.seed_item[0] = 0;
+      }
+    }
+  }
+  __syncthreads();
+
+  for (;;) {
+    // ============================ EVAL phase (+ pending acceptance of the previous round)
+    const int32_t rid = s_rid + 1;
+    const int slot = rid % 3;
+    const int32_t psize = s_psize, pos = s_pos, g = s_g;
+    const double cap = s_cap;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.ctrl[3 + (rid + 1) % 3] = 0;  // list written 2 phases ago, read last phase: reusable next phase
+      if (s_pending_seed >= 0) a.group_of_item[s_pending_seed] = g;
+    }
+    if (s_acc_cnt > 0) {
+      const int32_t* cj = a.cand_j + (size_t)s_acc_list * m;
+      const uint8_t* co = a.cand_ok + (size_t)s_acc_list * m;
+      for (int64_t i = gtid; i < s_acc_cnt; i += gthreads) {
+        const int32_t j = __ldcg(cj + i);
+        if (__ldcg(co + i) && j <= s_acc_limit) a.group_of_item[j] = s_acc_g;
+      }
+    }
+    if (threadIdx.x == 0) s_js = INT_MAX;
+    // ---- prefix selection
+    int32_t t;
+    if (!a.cosine) {
+      t = (int32_t)ceil(__dmul_rn(tau, (double)psize));
+    } else {
+      t = (int32_t)ceil(__dmul_rn(__dmul_rn(__dmul_rn(tau, tau), (double)psize), 1.0 - 1e-12));
+    }
+    const int mode = (t >= 1 && psize > 0) ? 0 : (psize == 0 && tau > 0.0) ? 1 : 2;
+    if (mode == 0) {
+      if (threadIdx.x < 33) s_hist[threadIdx.x] = 0;
+      __syncthreads();
+      for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
+        const int32_t sg = plist[q];
+        const int64_t len = a.post_ptr[sg + 1] - a.post_ptr[sg];
+        atomicAdd(&s_hist[63 - __clzll((long long)(len > 1 ? len : (int64_t)1))], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int32_t npre = psize - t + 1;
+        int32_t cum = 0, b = 0;
+        for (; b < 33; ++b) {
+          cum += s_hist[b];
+          if (cum >= npre) break;
+        }
+        s_bstar = b;
+      }
+      __syncthreads();
+      const int32_t bstar = s_bstar;
+      for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
+        const int32_t sg = plist[q];
+        const int64_t lo0 = a.post_ptr[sg], hi0 = a.post_ptr[sg + 1];
+        int32_t len_rem = 0, start = 0;
+        if (63 - __clzll((long long)((hi0 - lo0) > 1 ? (hi0 - lo0) : (int64_t)1)) <= bstar) {
+          int64_t lo = lo0, hi = hi0;  // first posting >= pos
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (a.post_item[mid] < pos) lo = mid + 1;
+            else hi = mid;
+          }
+          start = (int32_t)lo;
+          len_rem = (int32_t)(hi0 - lo);
+        }
+        pstart[q] = start;
+        pscan[q] = len_rem;
+      }
+      __syncthreads();
+      const int32_t T = block_exclusive_scan(pscan, psize, s_w, &s_carry);
+      if (threadIdx.x == 0) s_T = T;
+      __syncthreads();
+    } else {
+      __syncthreads();
+    }
+    // ---- enumerate + evaluate; candidates appended (warp-aggregated) to list rid % 3
+    int32_t my_js = INT_MAX;
+    {
+      int32_t* cj = a.cand_j + (size_t)slot * m;
+      uint8_t* co = a.cand_ok + (size_t)slot * m;
+      int64_t total;
+      if (mode == 0) total = s_T;
+      else if (mode == 1) total = __ldg(a.n_empty);
+      else total = m - pos;
+      int32_t emp_lo = 0;
+      if (mode == 1) {  // first empty item >= pos
+        int32_t lo = 0, hi = __ldg(a.n_empty);
+        while (lo < hi) {
+          const int32_t mid = (lo + hi) >> 1;
+          if (a.empties[mid] < pos) lo = mid + 1;
+          else hi = mid;
+        }
+        emp_lo = lo;
+        total -= lo;
+      }
+      for (int64_t e0 = 0; e0 < total; e0 += gthreads) {
+        const int64_t e = e0 + gtid;
+        bool has = false, ok = false;
+        int32_t j = -1;
+        if (e < total) {
+          if (mode == 0) {
+            int32_t lo = 0, hi = psize;  // last q with pscan[q] <= e
+            while (hi - lo > 1) {
+              const int32_t mid = (lo + hi) >> 1;
+              if (pscan[mid] <= e) lo = mid;
+              else hi = mid;
+            }
+            j = a.post_item[pstart[lo] + (e - pscan[lo])];
+          } else if (mode == 1) {
+            j = a.empties[emp_lo + e];
+          } else {
+            j = pos + (int32_t)e;
+          }
+          if (__ldcg(a.group_of_item + j) < 0 && (mode == 2 || atomicExch(a.stamp + j, rid) != rid)) {
+            has = true;
+            const int64_t p0 = a.item_ptr[j], p1 = a.item_ptr[j + 1];
+            int64_t inter = 0;
+            for (int64_t p = p0; p < p1; ++p) {
+              const int32_t sg = a.item_seg[p];
+              inter += (sP[sg >> 6] >> (sg & 63)) & 1ull;
+            }
+            const int64_t sz = p1 - p0;
+            ok = accept_dev(inter, psize, sz, tau, a.cosine, a.bounded, cap);
+            if (ok && a.update && inter < sz) my_js = min(my_js, j);
+          }
+        }
+        const unsigned act = __activemask();
+        const unsigned ball = __ballot_sync(act, has);
+        if (ball) {
+          const int leader = __ffs(act) - 1;
+          int32_t base = 0;
+          if (lane == leader) base = atomicAdd(a.ctrl + 3 + slot, __popc(ball));
+          base = __shfl_sync(act, base, leader);
+          if (has) {
+            const int32_t idx = base + __popc(ball & ((1u << lane) - 1u));
+            cj[idx] = j;
+            co[idx] = ok ? 1 : 0;
+          }
+        }
+      }
+    }
+    my_js = __reduce_min_sync(__activemask(), my_js);
+    if (lane == 0 && my_js != INT_MAX) atomicMin(&s_js, my_js);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_js != INT_MAX) atomicMin(a.ctrl + slot, s_js);
+    grid_barrier(a.ctrl + 8, a.ctrl + 9);
+
+    const int32_t js = *((volatile int32_t*)(a.ctrl + slot));
+    const int32_t ccnt = *((volatile int32_t*)(a.ctrl + 3 + slot));
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl[(rid + 2) % 3] = INT_MAX;
+    if (threadIdx.x == 0) {
+      s_rid = rid;
+      s_pending_seed = -1;
+      s_acc_list = slot;
+      s_acc_cnt = ccnt;
+      s_acc_g = g;
+    }
+    if (js < m) {
+      // ---- growth at js: OR its segments into P (appending new ones to plist in list order)
+      if (threadIdx.x < 32) {
+        const int64_t p0 = a.item_ptr[js], p1 = a.item_ptr[js + 1];
+        int c = 0;
+        for (int64_t p = p0 + lane; p < p1; p += 32) {
+          const int32_t sg = a.item_seg[p];
+          c += (int)((sP[sg >> 6] >> (sg & 63)) & 1ull);
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) s_inter = c;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int64_t p0 = a.item_ptr[js], p1 = a.item_ptr[js + 1];
+        int32_t ps = psize;
+        for (int64_t p = p0; p < p1; ++p) {
+          const int32_t sg = a.item_seg[p];
+          const unsigned long long bit = 1ull << (sg & 63);
+          if (!(sP[sg >> 6] & bit)) {
+            sP[sg >> 6] |= bit;
+            plist[ps++] = sg;
+          }
+        }
+        s_psize = ps;  // = psize + size(js) - inter(js)
+        s_pos = js + 1;
+        s_acc_limit = js;
+      }
+      __syncthreads();
+      continue;
+    }
+    // ============================ ACCEPT phase (group complete: all ok candidates of the last round)
+    if (threadIdx.x == 0) s_acc_limit = INT_MAX;
+    __syncthreads();
+    {
+      const int32_t* cj = a.cand_j + (size_t)slot * m;
+      const uint8_t* co = a.cand_ok + (size_t)slot * m;
+      for (int64_t i = gtid; i < ccnt; i += gthreads) {
+        const int32_t j = __ldcg(cj + i);
+        if (__ldcg(co + i)) a.group_of_item[j] = g;
+      }
+    }
+    grid_barrier(a.ctrl + 8, a.ctrl + 9);
+    // ============================ SEED: first unassigned item after the seed (same in every block)
+    if (threadIdx.x < 32) {
+      int32_t j0 = s_seed + 1;
+      int32_t found = m;
+      for (; j0 < m; j0 += 32) {
+        const int32_t j = j0 + lane;
+        const bool un = j < m && __ldcg(a.group_of_item + j) < 0;
+        const unsigned b = __ballot_sync(0xffffffffu, un);
+        if (b) {
+          found = j0 + __ffs(b) - 1;
+          break;
+        }
+      }
+      if (lane == 0) s_next = found;
+    }
+    __syncthreads();
+    const int32_t nxt = s_next;
+    if (nxt >= m) break;
+    // reset P to the new seed's pattern
+    for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
+      const int32_t sg = plist[q];
+      atomicAnd(&sP[sg >> 6], ~(1ull << (sg & 63)));
+    }
+    __syncthreads();
+    {
+      const int64_t p0 = a.item_ptr[nxt], len = a.item_ptr[nxt + 1] - p0;
+      for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
+        const int32_t sg = a.item_seg[p0 + k];
+        plist[k] = sg;
+        atomicOr(&sP[sg >> 6], 1ull << (sg & 63));
+      }
+      if (threadIdx.x == 0) {
+        s_psize = (int32_t)len;
+        s_cap = __ddiv_rn((double)len, cap_den);
+        s_pos = nxt + 1;
+        s_seed = nxt;
+        s_g = g + 1;
+        s_acc_cnt = 0;
+        s_pending_seed = nxt;  // written after the next barrier (other CTAs may still be scanning)
+        if (blockIdx.x == 0) a.seed_item[g + 1] = nxt;
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl[6] = s_g + 1;
+}
+
+// patterns of the sparse path: unique (group, segment) pairs of all member items
+__global__ void pattern_pairs_kernel(const int32_t* __restrict__ group_of_item, const int64_t* __restrict__ item_ptr,
+                                     const int32_t* __restrict__ item_seg, int64_t m, int64_t n_seg,
+                                     unsigned long long* keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < m; j += warps) {
+    const unsigned long long g = (unsigned long long)group_of_item[j];
+    for (int64_t p = item_ptr[j] + lane; p < item_ptr[j + 1]; p += 32)
+      keys[p] = g * (unsigned long long)n_seg + (unsigned long long)item_seg[p];
+  }
+}
+
+__global__ void pattern_emit_kernel(const unsigned long long* __restrict__ ukeys, const int* __restrict__ n_unique,
+                                    int64_t n_seg, int64_t* pattern_idx, int32_t* gcnt) {
+  const int64_t U = *n_unique;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < U; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ukeys[i];
+    pattern_idx[i] = (int64_t)(k % (unsigned long long)n_seg);
+    atomicAdd(gcnt + (int64_t)(k / (unsigned long long)n_seg), 1);
+  }
+}
+
+
+__global__ void widen_i32_kernel(const int32_t* __restrict__ in, int64_t n, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64_t* col_idx, const int64_t* boundaries,
+                     int64_t n_seg, int32_t delta, double tau, int similarity, int bounded, int pattern_update,
+                     int use_compression, void* workspace, size_t ws_bytes, int64_t* group_of, int64_t* row_perm,
+                     int64_t* group_ptr, int64_t* seed_size, int64_t* pattern_ptr, int64_t* pattern_idx,
+                     int64_t* n_groups, cudaStream_t stream) {
+  SWs ws = carve_sparse(workspace, n, nnz, n_seg);
+  if (ws_bytes < ws.total) return fail(RB_EINVAL, "workspace too small");
+  const int64_t W = words_of(n_seg);
+  int rc = narrow_bounds(boundaries, n_seg, ws.b32, stream);
+  if (rc) return rc;
+  SegMap seg{ws.b32, (int32_t)n_seg, delta};
+  const unsigned g1 = grid_for(n, 256);
+  size_t tb;
+  // ---- K1: row segment lists
+  seg_count_kernel<<<grid_for(n, 8), 256, 0, stream>>>(row_ptr, col_idx, n, seg, ws.sizes);
+  widen_i32_kernel<<<g1, 256, 0, stream>>>(ws.sizes, n, ws.pcnt);
+  RB_CUDA_TRY(cudaMemsetAsync(ws.pcnt + n, 0, sizeof(int64_t), stream));
+  tb = ws.cub_bytes;
+  RB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.cub_tmp, tb, ws.pcnt, ws.rs_ptr, (int)(n + 1), stream));
+  seg_write_kernel<<<grid_for(n, 8), 256, 0, stream>>>(row_ptr, col_idx, n, seg, ws.rs_ptr, ws.rs);
+  RB_CUDA_TRY(cudaGetLastError());
+  // ---- K2: compression on the exact lists
+  int32_t m = (int32_t)n;
+  if (use_compression) {
+    list_hash_kernel<<<g1, 256, 0, stream>>>(ws.rs_ptr, ws.rs, n, ws.keys_a, ws.vals_a);
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, tb, ws.keys_a, ws.keys_b, ws.vals_a, ws.vals_b, (int)n, 0,
+                                                64, stream));
+    run_head_kernel<<<g1, 256, 0, stream>>>(ws.keys_b, n, ws.t0);
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceScan::InclusiveScan(ws.cub_tmp, tb, ws.t0, ws.t1, MaxOp(), (int)n, stream));
+    list_rep_kernel<<<g1, 256, 0, stream>>>(ws.rs_ptr, ws.rs, ws.vals_b, ws.t1, n, ws.t0);
+    is_rep_kernel<<<g1, 256, 0, stream>>>(ws.t0, n, ws.t1);
+    RB_CUDA_TRY(cudaMemsetAsync(ws.t1 + n, 0, sizeof(int32_t), stream));
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.cub_tmp, tb, ws.t1, ws.vals_a, (int)(n + 1), stream));
+    items_kernel<<<g1, 256, 0, stream>>>(ws.t0, ws.vals_a, n, ws.item_of_row, ws.reps);
+    RB_CUDA_TRY(cudaMemcpyAsync(&m, ws.vals_a + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  } else {
+    identity_items_kernel<<<g1, 256, 0, stream>>>(n, ws.item_of_row, ws.reps);
+  }
+  // ---- item lists + inverted index
+  const unsigned gm = grid_for(m, 256);
+  item_size_kernel<<<gm, 256, 0, stream>>>(ws.reps, ws.sizes, m, ws.item_size, ws.group_of_item, ws.stamp);
+  widen_i32_kernel<<<gm, 256, 0, stream>>>(ws.item_size, m, ws.pcnt);
+  RB_CUDA_TRY(cudaMemsetAsync(ws.pcnt + m, 0, sizeof(int64_t), stream));
+  tb = ws.cub_bytes;
+  RB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.cub_tmp, tb, ws.pcnt, ws.item_ptr, (int)(m + 1), stream));
+  RB_CUDA_TRY(cudaMemsetAsync(ws.seg_cnt, 0, sizeof(int32_t) * (n_seg + 1), stream));
+  item_lists_kernel<<<grid_for(m, 8), 256, 0, stream>>>(ws.reps, ws.rs_ptr, ws.rs, ws.item_ptr, m, ws.item_seg,
+                                                        ws.seg_cnt, ws.keys_a);
+  int64_t E = 0;
+  RB_CUDA_TRY(cudaMemcpyAsync(&E, ws.item_ptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  widen_i32_kernel<<<grid_for(n_seg + 1, 256), 256, 0, stream>>>(ws.seg_cnt, n_seg + 1, ws.pcnt);
+  tb = ws.cub_bytes;
+  RB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.cub_tmp, tb, ws.pcnt, ws.post_ptr, (int)(n_seg + 1), stream));
+  if (E > 0) {
+    int end_bit = 32;
+    while (end_bit < 64 && ((unsigned long long)n_seg >> (end_bit - 32)) != 0) ++end_bit;
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(ws.cub_tmp, tb, ws.keys_a, ws.keys_b, (int)E, 0, end_bit, stream));
+    postings_kernel<<<grid_for(E, 256), 256, 0, stream>>>(ws.keys_b, E, ws.post_item);
+  }
+  empties_kernel<<<1, 1024, 0, stream>>>(ws.item_size, m, ws.empties, ws.n_empty);
+  RB_CUDA_TRY(cudaGetLastError());
+  // ---- K3: pruned greedy scan
+  {
+    int32_t ctrl0[32];
+    for (int i = 0; i < 32; ++i) ctrl0[i] = 0;
+    for (int i = 0; i < 3; ++i) ctrl0[i] = INT_MAX;
+    RB_CUDA_TRY(cudaMemcpyAsync(ws.ctrl, ctrl0, sizeof(ctrl0), cudaMemcpyHostToDevice, stream));
+    SGreedyArgs ga;
+    ga.m = m;
+    ga.n_seg = (int32_t)n_seg;
+    ga.W = (int32_t)W;
+    ga.item_ptr = ws.item_ptr;
+    ga.item_seg = ws.item_seg;
+    ga.item_size = ws.item_size;
+    ga.post_ptr = ws.post_ptr;
+    ga.post_item = ws.post_item;
+    ga.empties = ws.empties;
+    ga.n_empty = ws.n_empty;
+    ga.tau = tau;
+    ga.cosine = similarity == RB_COSINE;
+    ga.bounded = bounded != 0;
+    ga.update = pattern_update != 0;
+    ga.group_of_item = ws.group_of_item;
+    ga.stamp = ws.stamp;
+    ga.cand_j = ws.cand_j;
+    ga.cand_ok = ws.cand_ok;
+    ga.seed_item = ws.seed_item;
+    ga.ctrl = ws.ctrl;
+    ga.scratch = ws.scratch;
+    const size_t shm = sizeof(uint64_t) * W;
+    if (shm > 200 * 1024) return fail(RB_EUNSUPPORTED, "too many segments for the pattern bitset in shared memory");
+    void* fn = (void*)sparse_greedy_kernel;
+    if (shm > 48 * 1024) RB_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    int blocks = 1;
+    if ((int64_t)m * 8 > 64 * 1024 || E > 256 * 1024) {
+      int dev = 0, per_sm = 0, sms = 0;
+      RB_CUDA_TRY(cudaGetDevice(&dev));
+      RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      RB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSparseThreads, shm));
+      if (per_sm < 1) return fail(RB_ECUDA, "sparse greedy kernel cannot be resident");
+      blocks = std::min(sms, kSparseBlocks);
+    }
+    void* args[] = {&ga};
+    RB_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kSparseThreads), args, shm, stream));
+  }
+  int32_t H32 = 0;
+  RB_CUDA_TRY(cudaMemcpyAsync(&H32, ws.ctrl + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+  RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  const int64_t H = H32;
+  // ---- assembly (as the dense path)
+  assembly_keys_kernel<<<g1, 256, 0, stream>>>(ws.item_of_row, ws.group_of_item, n, m, ws.keys_a, ws.vals_a);
+  {
+    int end_bit = 1;
+    while (end_bit < 64 && ((unsigned long long)H * (unsigned long long)m) > (1ull << end_bit)) ++end_bit;
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, tb, ws.keys_a, ws.keys_b, ws.vals_a, ws.vals_b, (int)n, 0,
+                                                end_bit, stream));
+  }
+  assembly_out_kernel<<<g1, 256, 0, stream>>>(ws.vals_b, ws.keys_b, n, m, H, row_perm, group_of, group_ptr);
+  seed_size_kernel<<<grid_for(H, 256), 256, 0, stream>>>(ws.seed_item, ws.item_size, H, seed_size);
+  // ---- patterns: sorted unique (group, segment) pairs
+  RB_CUDA_TRY(cudaMemsetAsync(ws.t1, 0, sizeof(int32_t) * (H + 1), stream));
+  if (E > 0) {
+    pattern_pairs_kernel<<<grid_for(m, 8), 256, 0, stream>>>(ws.group_of_item, ws.item_ptr, ws.item_seg, m, n_seg,
+                                                             ws.keys_a);
+    int end_bit = 1;
+    while (end_bit < 64 && ((unsigned long long)H * (unsigned long long)n_seg) > (1ull << end_bit)) ++end_bit;
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(ws.cub_tmp, tb, ws.keys_a, ws.keys_b, (int)E, 0, end_bit, stream));
+    tb = ws.cub_bytes;
+    RB_CUDA_TRY(cub::DeviceSelect::Unique(ws.cub_tmp, tb, ws.keys_b, ws.keys_a, (int*)ws.t0, (int)E, stream));
+    pattern_emit_kernel<<<grid_for(E, 256), 256, 0, stream>>>(ws.keys_a, (const int*)ws.t0, n_seg, pattern_idx, ws.t1);
+  }
+  widen_i32_kernel<<<grid_for(H + 1, 256), 256, 0, stream>>>(ws.t1, H + 1, ws.pcnt);
+  tb = ws.cub_bytes;
+  RB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws.cub_tmp, tb, ws.pcnt, pattern_ptr, (int)(H + 1), stream));
+  RB_CUDA_TRY(cudaGetLastError());
+  *n_groups = H;
+  return RB_OK;
+}
 }  // namespace
 }  // namespace rb
 
@@ -495,10 +1263,10 @@ using namespace rb;
 
 extern "C" int rb_block_1sa_workspace_size(int64_t n_rows, int64_t nnz, int64_t n_seg, int use_compression,
                                            size_t* bytes) {
-  (void)nnz;
   (void)use_compression;
-  if (!bytes || n_rows < 0 || n_seg < 0) return fail(RB_EINVAL, "bad arguments");
-  *bytes = carve(nullptr, n_rows, words_of(n_seg), n_seg).total;
+  if (!bytes || n_rows < 0 || n_seg < 0 || nnz < 0) return fail(RB_EINVAL, "bad arguments");
+  *bytes = use_sparse_path(words_of(n_seg)) ? carve_sparse(nullptr, n_rows, nnz, n_seg).total
+                                            : carve(nullptr, n_rows, words_of(n_seg), n_seg).total;
   return RB_OK;
 }
 
@@ -508,15 +1276,12 @@ extern "C" int rb_block_1sa(int64_t n, int64_t n_cols, int64_t nnz, const int64_
                             int64_t* group_of, int64_t* row_perm, int64_t* group_ptr, int64_t* seed_size,
                             int64_t* pattern_ptr, int64_t* pattern_idx, int64_t* n_groups, void* stream_) {
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  (void)nnz;
   // MergePolicy validation (blocking.py:80-84)
   if (similarity != RB_JACCARD && similarity != RB_COSINE) return fail(RB_EINVAL, "unknown similarity");
   if (!(tau >= 0.0 && tau <= 1.0)) return fail(RB_EINVAL, "tau must be in [0, 1]");
   if (n < 0 || !n_groups) return fail(RB_EINVAL, "bad arguments");
   if (n >= (int64_t(1) << 31)) return fail(RB_EUNSUPPORTED, "n_rows must be < 2^31");
   const int64_t W = words_of(n_seg);
-  Ws ws = carve(workspace, n, W, n_seg);
-  if (ws_bytes < ws.total) return fail(RB_EINVAL, "workspace too small");
   int32_t delta = 0, maxw = 0;
   int rc = inspect_boundaries(boundaries, n_seg, n_cols, &delta, &maxw, nullptr, stream);
   if (rc) return rc;
@@ -526,6 +1291,12 @@ extern "C" int rb_block_1sa(int64_t n, int64_t n_cols, int64_t nnz, const int64_
     RB_CUDA_TRY(cudaMemsetAsync(pattern_ptr, 0, sizeof(int64_t), stream));
     return RB_OK;
   }
+  if (use_sparse_path(W))
+    return block_1sa_sparse(n, nnz, row_ptr, col_idx, boundaries, n_seg, delta, tau, similarity, bounded,
+                            pattern_update, use_compression, workspace, ws_bytes, group_of, row_perm, group_ptr,
+                            seed_size, pattern_ptr, pattern_idx, n_groups, stream);
+  Ws ws = carve(workspace, n, W, n_seg);
+  if (ws_bytes < ws.total) return fail(RB_EINVAL, "workspace too small");
   rc = narrow_bounds(boundaries, n_seg, ws.b32, stream);
   if (rc) return rc;
   SegMap seg{ws.b32, (int32_t)n_seg, delta};

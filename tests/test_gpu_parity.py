@@ -231,3 +231,22 @@ def test_errors_map_to_reference_exceptions():
         rb.spmm_vbr(V, rb.DenseMatrix.zeros(5, 2))
     with pytest.raises(ValueError):
         rb.MergePolicy(tau=1.5)
+
+
+@pytest.fixture
+def force_sparse_1sa(monkeypatch):
+    monkeypatch.setenv("RB_1SA_MODE", "sparse")
+
+
+def test_block_1sa_sparse_path_bit_exact_golden(golden_small, force_sparse_1sa):
+    """The inverted-index (pruned) greedy used for large W is exact on every golden case."""
+    for name, case in golden_small.items():
+        g = rb.block_1sa(csr_of(case), part_of(case), policy_of(case), bool(case["use_compression"]))
+        check_grouping(g, case, name)
+
+
+@pytest.mark.parametrize("name", MEDIUM)
+def test_block_1sa_sparse_path_medium(name, force_sparse_1sa):
+    case = load_golden(name)
+    g = rb.block_1sa(csr_of(case), part_of(case), policy_of(case), bool(case["use_compression"]))
+    check_grouping(g, case, name)

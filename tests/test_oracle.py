@@ -67,3 +67,19 @@ def test_oracle_structure_medium(name):
         r = np.random.default_rng(7).standard_normal(B.shape[1])
         np.testing.assert_allclose(C @ r, case["C_dot_r"], rtol=1e-9, atol=1e-9)
         np.testing.assert_allclose(C.sum(axis=1), case["C_rowsum"], rtol=1e-12, atol=1e-12)
+
+
+def test_pruned_oracle_matches_golden(golden_small):
+    """orc_block_1sa_pruned (the config-3-scale oracle) == the reference on every golden case."""
+    from conftest import load_golden
+    cases = list(golden_small.items()) + [(m, load_golden(m)) for m in MEDIUM]
+    for name, c in cases:
+        a = oracle.block_1sa_arrays(c["row_ptr"], c["col_idx"], c["boundaries"], tau=float(c["tau"]),
+                                    similarity="cosine" if int(c["cosine"]) else "jaccard",
+                                    bounded=bool(c["bounded"]), pattern_update=bool(c["pattern_update"]),
+                                    use_compression=bool(c["use_compression"]), pruned=True)
+        assert np.array_equal(a["row_perm"], c["row_perm"]), name
+        assert np.array_equal(a["group_ptr"], c["row_partition"]), name
+        assert np.array_equal(a["seed_size"], c["seed_size"]), name
+        assert np.array_equal(a["pattern_ptr"], c["pattern_ptr"]), name
+        assert np.array_equal(a["pattern_idx"], c["pattern_idx"]), name
