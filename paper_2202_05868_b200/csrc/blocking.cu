@@ -536,7 +536,8 @@ struct SWs {
   int32_t* cand_j;         // [3*n]
   uint8_t* cand_ok;        // [3*n]
   int32_t* seed_item;      // [n]
-  int32_t* ctrl;           // [32]
+  int32_t* ctrl;           // [16 + 2*blocks]
+  unsigned long long* stats;  // [8]
   int32_t* scratch;        // [blocks * 3 * (n_seg+1)]
   int64_t* pcnt;           // [n+1]
   int32_t* b32;            // [n_seg+1]
@@ -595,7 +596,8 @@ SWs carve_sparse(void* base, int64_t n, int64_t nnz, int64_t n_seg) {
   w.cand_j = (int32_t*)take(4 * 3 * n1);
   w.cand_ok = (uint8_t*)take(3 * n1);
   w.seed_item = (int32_t*)take(4 * n1);
-  w.ctrl = (int32_t*)take(4 * 32);
+  w.ctrl = (int32_t*)take(4 * (16 + 2 * kSparseBlocks));
+  w.stats = (unsigned long long*)take(8 * 8);
   w.scratch = (int32_t*)take(4 * (size_t)kSparseBlocks * 3 * (s1 + 1));
   w.pcnt = (int64_t*)take(8 * (n1 + 1));
   w.b32 = (int32_t*)take(4 * s1);
@@ -753,18 +755,54 @@ struct SGreedyArgs {
   int32_t* cand_j;   // [3][m]
   uint8_t* cand_ok;  // [3][m]
   int32_t* seed_item;
-  int32_t* ctrl;     // [0..2] jstar slots, [3..5] candidate counts, [6] H, [8] count, [9] gen
-  int32_t* scratch;  // per block: plist | pscan | pstart, each n_seg+1
+  int32_t* ctrl;     // [0..2] first growing hit, [3..5] candidate counts, [6] H, [8] count, [9] gen,
+                     // [10..12] accepted-candidate counts, [16..16+2*kSparseBlocks) speculative flags
+  int32_t* scratch;  // per block: overflow of the pattern list arrays, 3 x (n_seg+1)
+  unsigned long long* stats;  // [8] counters (block 0): batches, batch seeds, singletons, rounds, accepts,
+                              //     cycles in BATCH, cycles in GROUP, batch-skips
 };
 
-// block-wide exclusive scan of v over n elements stored in global scratch (in place), returns total
-__device__ int32_t block_exclusive_scan(int32_t* v, int32_t n, int32_t* smem_w /*[32]*/, int32_t* smem_carry) {
+constexpr int kPlistSmem = 4096;
+constexpr int64_t kBatchMaxEnum = 4 * kSparseThreads;  // speculative CTA enumerates at most this many entries  // pattern-list entries held in shared memory (the rest in scratch)
+
+// The pattern's segment list and its prefix-enumeration arrays (start, exclusive-scan of lengths).
+struct PList {
+  int32_t* sm;  // [3][kPlistSmem]
+  int32_t* gm;  // [3][n1]
+  int32_t n1;
+  __device__ __forceinline__ int32_t& seg(int32_t q) { return q < kPlistSmem ? sm[q] : gm[q]; }
+  __device__ __forceinline__ int32_t& scan(int32_t q) { return q < kPlistSmem ? sm[kPlistSmem + q] : gm[n1 + q]; }
+  __device__ __forceinline__ int32_t& start(int32_t q) {
+    return q < kPlistSmem ? sm[2 * kPlistSmem + q] : gm[2 * n1 + q];
+  }
+};
+
+// warp-cooperative lower_bound (32-ary search): first index in [lo, hi) with arr[idx] >= key
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ arr, int64_t lo, int64_t hi,
+                                                    int32_t key, int lane) {
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t idx = lo + lane * step;
+    const bool less = idx < hi && __ldg(arr + idx) < key;
+    const int c = __popc(__ballot_sync(0xffffffffu, less));
+    if (c == 0) return lo;
+    const int64_t nlo = lo + (int64_t)(c - 1) * step + 1;
+    hi = min(hi, lo + (int64_t)c * step);
+    lo = nlo;
+  }
+  const int64_t idx = lo + lane;
+  const bool less = idx < hi && __ldg(arr + idx) < key;
+  return lo + __popc(__ballot_sync(0xffffffffu, less));
+}
+
+// block-wide exclusive scan of pl.scan(0..n), returns the total
+__device__ int32_t block_scan_plist(PList& pl, int32_t n, int32_t* smem_w /*[32]*/, int32_t* smem_carry) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x == 0) *smem_carry = 0;
   __syncthreads();
   for (int32_t base = 0; base < n; base += blockDim.x) {
     const int32_t i = base + threadIdx.x;
-    const int32_t x = i < n ? v[i] : 0;
+    const int32_t x = i < n ? pl.scan(i) : 0;
     int32_t incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -780,12 +818,11 @@ __device__ int32_t block_exclusive_scan(int32_t* v, int32_t n, int32_t* smem_w /
         const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
         if (lane >= o) t += y;
       }
-      if (lane < nw) smem_w[lane] = t;  // inclusive warp totals
+      if (lane < nw) smem_w[lane] = t;
     }
     __syncthreads();
     const int32_t carry = *smem_carry;
-    const int32_t wbase = w > 0 ? smem_w[w - 1] : 0;
-    if (i < n) v[i] = carry + wbase + incl - x;
+    if (i < n) pl.scan(i) = carry + (w > 0 ? smem_w[w - 1] : 0) + incl - x;
     __syncthreads();
     if (threadIdx.x == 0) *smem_carry = carry + smem_w[nw - 1];
     __syncthreads();
@@ -793,171 +830,351 @@ __device__ int32_t block_exclusive_scan(int32_t* v, int32_t n, int32_t* smem_w /
   return *smem_carry;
 }
 
+struct BlockShared {
+  int32_t w[32], carry, hist[33], bstar, T, flag;
+};
+
+// Replace the block's pattern (bits in sP + list in pl) by item `it`'s segments; returns its size.
+__device__ int32_t load_pattern(const SGreedyArgs& a, unsigned long long* sP, PList& pl, int32_t old_psize,
+                                int32_t it) {
+  for (int32_t q = threadIdx.x; q < old_psize; q += blockDim.x) {
+    const int32_t sg = pl.seg(q);
+    atomicAnd(&sP[sg >> 6], ~(1ull << (sg & 63)));
+  }
+  __syncthreads();
+  const int64_t p0 = a.item_ptr[it];
+  const int32_t len = (int32_t)(a.item_ptr[it + 1] - p0);
+  for (int32_t k = threadIdx.x; k < len; k += blockDim.x) {
+    const int32_t sg = a.item_seg[p0 + k];
+    pl.seg(k) = sg;
+    atomicOr(&sP[sg >> 6], 1ull << (sg & 63));
+  }
+  __syncthreads();
+  return len;
+}
+
+// Enumeration set of one round: 0 = prefix postings, 1 = empty items, 2 = all items >= pos.
+// For mode 0 fills pl.start / pl.scan and returns the number of enumerated postings entries.
+__device__ int64_t prepare_round(const SGreedyArgs& a, PList& pl, BlockShared& bs, int32_t psize, int32_t pos,
+                                 int* mode_out, int32_t* emp_lo_out) {
+  const double tau = a.tau;
+  int32_t t;
+  if (!a.cosine) t = (int32_t)ceil(__dmul_rn(tau, (double)psize));
+  else t = (int32_t)ceil(__dmul_rn(__dmul_rn(__dmul_rn(tau, tau), (double)psize), 1.0 - 1e-12));
+  const int mode = (t >= 1 && psize > 0) ? 0 : (psize == 0 && tau > 0.0) ? 1 : 2;
+  *mode_out = mode;
+  *emp_lo_out = 0;
+  if (mode == 2) return a.m - pos;
+  if (mode == 1) {
+    int32_t lo = 0, hi = __ldg(a.n_empty);
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (a.empties[mid] < pos) lo = mid + 1;
+      else hi = mid;
+    }
+    *emp_lo_out = lo;
+    return __ldg(a.n_empty) - lo;
+  }
+  if (threadIdx.x < 33) bs.hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
+    const int32_t sg = pl.seg(q);
+    const int64_t len = a.post_ptr[sg + 1] - a.post_ptr[sg];
+    atomicAdd(&bs.hist[63 - __clzll((long long)(len > 1 ? len : 1))], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int32_t npre = psize - t + 1;
+    int32_t cum = 0, b = 0;
+    for (; b < 33; ++b) {
+      cum += bs.hist[b];
+      if (cum >= npre) break;
+    }
+    bs.bstar = b;
+  }
+  __syncthreads();
+  const int32_t bstar = bs.bstar;
+  for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {  // thread per pattern segment
+    const int32_t sg = pl.seg(q);
+    const int64_t lo0 = a.post_ptr[sg], hi0 = a.post_ptr[sg + 1];
+    int32_t rem = 0, st = 0;
+    if (63 - __clzll((long long)((hi0 - lo0) > 1 ? (hi0 - lo0) : 1)) <= bstar) {
+      int64_t lo = lo0, hi = hi0;  // first posting >= pos
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(a.post_item + mid) < pos) lo = mid + 1;
+        else hi = mid;
+      }
+      st = (int32_t)lo;
+      rem = (int32_t)(hi0 - lo);
+    }
+    pl.start(q) = st;
+    pl.scan(q) = rem;
+  }
+  __syncthreads();
+  const int32_t T = block_scan_plist(pl, psize, bs.w, &bs.carry);
+  if (threadIdx.x == 0) bs.T = T;
+  __syncthreads();
+  return bs.T;
+}
+
+__device__ __forceinline__ int32_t entry_item(const SGreedyArgs& a, PList& pl, int mode, int32_t psize, int64_t e,
+                                              int32_t pos, int32_t emp_lo) {
+  if (mode == 0) {
+    int32_t lo = 0, hi = psize;  // last q with scan(q) <= e
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (pl.scan(mid) <= e) lo = mid;
+      else hi = mid;
+    }
+    return a.post_item[pl.start(lo) + (e - pl.scan(lo))];
+  }
+  if (mode == 1) return a.empties[emp_lo + e];
+  return pos + (int32_t)e;
+}
+
+// |P ∩ segs(j)| with the pattern bits in shared memory; loads issued 8 at a time.
+__device__ __forceinline__ int64_t item_inter(const SGreedyArgs& a, const unsigned long long* sP, int64_t p0,
+                                              int64_t p1) {
+  int64_t inter = 0;
+  int64_t p = p0;
+  for (; p + 8 <= p1; p += 8) {
+    int32_t sg[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sg[k] = __ldg(a.item_seg + p + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) inter += (sP[sg[k] >> 6] >> (sg[k] & 63)) & 1ull;
+  }
+  for (; p < p1; ++p) {
+    const int32_t sg = __ldg(a.item_seg + p);
+    inter += (sP[sg >> 6] >> (sg & 63)) & 1ull;
+  }
+  return inter;
+}
+
+// Merge verdict for candidate j.  accept_dev is non-decreasing in inter and inter <= min(psize, size),
+// so a candidate that fails even with inter = min(psize, size) is rejected without reading its list.
+__device__ __forceinline__ bool eval_candidate(const SGreedyArgs& a, const unsigned long long* sP, int32_t j,
+                                               int64_t psize, double cap, bool* grows) {
+  const int64_t p0 = __ldg(a.item_ptr + j), p1 = __ldg(a.item_ptr + j + 1);
+  const int64_t sz = p1 - p0;
+  *grows = false;
+  if (!accept_dev(min(psize, sz), psize, sz, a.tau, a.cosine, a.bounded, cap)) return false;
+  const int64_t inter = item_inter(a, sP, p0, p1);
+  const bool ok = accept_dev(inter, psize, sz, a.tau, a.cosine, a.bounded, cap);
+  *grows = ok && a.update && inter < sz;
+  return ok;
+}
+
+// The greedy scan with speculative singleton batching (exact):
+//  BATCH: every CTA b takes the b-th unassigned item >= next as a speculative seed and tests whether
+//         ANY later unassigned item passes the merge test against it.  Seeds before the first one that
+//         has a hit are singleton groups in the sequential scan too (a singleton assigns only itself,
+//         which is not a candidate of any later seed), so they are committed in order at once.
+//  GROUP: the first seed with a hit runs the round protocol with all CTAs: enumerate + evaluate the
+//         candidates, reduce the first growing hit, accept the ok items before it, grow, repeat.
 __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyArgs a) {
-  extern __shared__ unsigned long long sP[];  // pattern bits, W words
-  __shared__ int32_t s_w[32], s_carry;
-  __shared__ int32_t s_hist[33];
-  __shared__ int32_t s_js, s_bstar, s_T, s_next, s_inter;
-  __shared__ int32_t s_psize, s_pos, s_seed, s_g, s_rid, s_acc_list, s_acc_cnt, s_acc_limit, s_acc_g, s_pending_seed;
+  extern __shared__ unsigned long long smem_dyn[];
+  unsigned long long* sP = smem_dyn;                                     // W words
+  int32_t* pl_sm = reinterpret_cast<int32_t*>(smem_dyn + a.W);           // 3 * kPlistSmem
+  __shared__ BlockShared bs;
+  __shared__ int32_t s_list[kSparseBlocks];
+  __shared__ int32_t s_list_len, s_f, s_js;
+  __shared__ int32_t s_mode, s_next, s_gnext, s_seed, s_g, s_pos, s_psize, s_rid, s_batch;
+  __shared__ int32_t s_acc_list, s_acc_cnt, s_acc_limit, s_acc_g;
+  __shared__ int32_t s_bpos, s_blen, s_grounds;  // batch cursor / length, rounds of the current group
   __shared__ double s_cap;
 
+  PList pl{pl_sm, a.scratch + (size_t)blockIdx.x * 3 * (a.n_seg + 1), a.n_seg + 1};
   const int32_t m = a.m;
   const double tau = a.tau;
   const double cap_den = __dsub_rn(1.0, __dmul_rn(0.5, tau));
-  int32_t* plist = a.scratch + (size_t)blockIdx.x * 3 * (a.n_seg + 1);
-  int32_t* pscan = plist + (a.n_seg + 1);
-  int32_t* pstart = pscan + (a.n_seg + 1);
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
 
   for (int w = threadIdx.x; w < a.W; w += blockDim.x) sP[w] = 0ull;
-  __syncthreads();
-  // seed item 0
-  {
-    const int64_t p0 = a.item_ptr[0], len = a.item_ptr[1] - p0;
-    for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
-      const int32_t sg = a.item_seg[p0 + k];
-      plist[k] = sg;
-      atomicOr(&sP[sg >> 6], 1ull << (sg & 63));
-    }
-    if (threadIdx.x == 0) {
-      s_psize = (int32_t)len;
-      s_cap = __ddiv_rn((double)len, cap_den);
-      s_pos = 1;
-      s_seed = 0;
-      s_g = 0;
-      s_rid = 0;
-      s_acc_cnt = 0;
-      s_pending_seed = -1;
-      if (blockIdx.x == 0) {
-        a.group_of_item[0] = 0;
-        a.seed_item[0] = 0;
-      }
-    }
+  if (threadIdx.x == 0) {
+    s_mode = 0;
+    s_next = 0;
+    s_gnext = 0;
+    s_psize = 0;
+    s_rid = 0;
+    s_batch = 0;
+    s_acc_cnt = 0;
+    s_bpos = 0;
+    s_blen = 0;
+    s_grounds = 0;
   }
   __syncthreads();
 
+  long long t_phase = clock64();
   for (;;) {
-    // ============================ EVAL phase (+ pending acceptance of the previous round)
+    if (s_mode == 0) {
+      // ============================ BATCH phase
+      t_phase = clock64();
+      if (threadIdx.x < 32) {
+        int32_t cnt = 0;
+        for (int32_t j0 = s_next; j0 < m && cnt < (int32_t)gridDim.x; j0 += 32) {
+          const int32_t j = j0 + lane;
+          const bool un = j < m && __ldcg(a.group_of_item + j) < 0;
+          const unsigned b = __ballot_sync(0xffffffffu, un);
+          const int32_t r = __popc(b & ((1u << lane) - 1u));
+          if (un && cnt + r < (int32_t)gridDim.x) s_list[cnt + r] = j;
+          cnt += __popc(b);
+        }
+        if (lane == 0) s_list_len = min(cnt, (int32_t)gridDim.x);
+      }
+      __syncthreads();
+      const int32_t len = s_list_len;
+      if (len == 0) break;
+      const int32_t batch = s_batch;
+      int32_t* flags = a.ctrl + 16 + (batch & 1) * kSparseBlocks;
+      const int32_t my = (int32_t)blockIdx.x < len ? s_list[blockIdx.x] : -1;
+      if (my >= 0) {
+        const int32_t psize = load_pattern(a, sP, pl, s_psize, my);
+        if (threadIdx.x == 0) {
+          s_psize = psize;
+          bs.flag = 0;
+        }
+        __syncthreads();
+        const double cap = __ddiv_rn((double)psize, cap_den);
+        int mode;
+        int32_t emp_lo;
+        const int64_t total = prepare_round(a, pl, bs, psize, my + 1, &mode, &emp_lo);
+        // a seed with a large candidate set is not tested speculatively by one CTA: reporting "unknown"
+        // (treated as a hit) ends the singleton run here and the GROUP protocol (all CTAs) takes it
+        if (total > kBatchMaxEnum && threadIdx.x == 0) bs.flag = 2;
+        __syncthreads();
+        for (int64_t e0 = 0; e0 < total && !bs.flag; e0 += blockDim.x) {
+          const int64_t e = e0 + threadIdx.x;
+          if (e < total) {
+            const int32_t j = entry_item(a, pl, mode, psize, e, my + 1, emp_lo);
+            if (__ldcg(a.group_of_item + j) < 0) {
+              bool grows;
+              if (eval_candidate(a, sP, j, psize, cap, &grows)) bs.flag = 1;
+            }
+          }
+          __syncthreads();
+          if (bs.flag) break;  // uniform: read after the barrier
+        }
+        if (threadIdx.x == 0) flags[blockIdx.x] = bs.flag;
+      }
+      grid_barrier(a.ctrl + 8, a.ctrl + 9);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.stats[0] += 1;
+        a.stats[1] += len;
+        a.stats[5] += clock64() - t_phase;
+      }
+      if (threadIdx.x == 0) {
+        s_bpos = 0;
+        s_blen = len;
+        s_batch = batch + 1;
+        s_mode = 2;
+      }
+      __syncthreads();
+    }
+    if (s_mode == 2) {
+      // ============================ consume the batch verdicts from s_bpos (no barrier needed: every
+      // CTA reads the same flags and commits nothing that any CTA reads again)
+      const int32_t len = s_blen, bpos = s_bpos;
+      const int32_t* flags = a.ctrl + 16 + ((s_batch - 1) & 1) * kSparseBlocks;
+      if (threadIdx.x < 32) {
+        int32_t f = len;
+        for (int32_t k0 = bpos; k0 < len; k0 += 32) {
+          const int32_t k = k0 + lane;
+          const bool hit = k < len && *((volatile const int32_t*)(flags + k)) != 0;
+          const unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (b) {
+            f = k0 + __ffs(b) - 1;
+            break;
+          }
+        }
+        if (lane == 0) s_f = f;
+      }
+      __syncthreads();
+      const int32_t f = s_f, g0 = s_gnext;
+      if (blockIdx.x == 0) {  // singletons before the first hit (nobody reads items < the next seed again)
+        for (int32_t k = bpos + threadIdx.x; k < f; k += blockDim.x) {
+          a.group_of_item[s_list[k]] = g0 + (k - bpos);
+          a.seed_item[g0 + (k - bpos)] = s_list[k];
+        }
+        if (threadIdx.x == 0) a.stats[2] += f - bpos;
+      }
+      __syncthreads();
+      if (f == len) {
+        if (threadIdx.x == 0) {
+          s_gnext = g0 + (f - bpos);
+          s_next = s_list[len - 1] + 1;
+          s_mode = 0;
+        }
+        __syncthreads();
+        continue;
+      }
+      // the seed with a hit (or too large to test speculatively) starts a GROUP on all CTAs
+      const int32_t seed = s_list[f];
+      const int32_t gid = g0 + (f - bpos);
+      const int32_t psize = load_pattern(a, sP, pl, s_psize, seed);
+      if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+          a.group_of_item[seed] = gid;
+          a.seed_item[gid] = seed;
+        }
+        s_seed = seed;
+        s_g = gid;
+        s_gnext = gid + 1;
+        s_psize = psize;
+        s_cap = __ddiv_rn((double)psize, cap_den);
+        s_pos = seed + 1;
+        s_acc_cnt = 0;
+        s_bpos = f + 1;
+        s_grounds = 0;
+        s_mode = 1;
+      }
+      __syncthreads();
+      continue;
+    }
+
+    // ============================ GROUP: EVAL round (+ acceptance of the previous round)
+    t_phase = clock64();
     const int32_t rid = s_rid + 1;
     const int slot = rid % 3;
     const int32_t psize = s_psize, pos = s_pos, g = s_g;
     const double cap = s_cap;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.ctrl[3 + (rid + 1) % 3] = 0;  // list written 2 phases ago, read last phase: reusable next phase
-      if (s_pending_seed >= 0) a.group_of_item[s_pending_seed] = g;
+      a.ctrl[3 + (rid + 1) % 3] = 0;   // candidate list of 2 rounds ago is free again
+      a.ctrl[10 + (rid + 1) % 3] = 0;
     }
     if (s_acc_cnt > 0) {
       const int32_t* cj = a.cand_j + (size_t)s_acc_list * m;
       const uint8_t* co = a.cand_ok + (size_t)s_acc_list * m;
-      for (int64_t i = gtid; i < s_acc_cnt; i += gthreads) {
+      const int32_t lim = s_acc_limit, ag = s_acc_g, cnt = s_acc_cnt;
+      for (int64_t i = gtid; i < cnt; i += gthreads) {
         const int32_t j = __ldcg(cj + i);
-        if (__ldcg(co + i) && j <= s_acc_limit) a.group_of_item[j] = s_acc_g;
+        if (__ldcg(co + i) && j <= lim) a.group_of_item[j] = ag;
       }
     }
     if (threadIdx.x == 0) s_js = INT_MAX;
-    // ---- prefix selection
-    int32_t t;
-    if (!a.cosine) {
-      t = (int32_t)ceil(__dmul_rn(tau, (double)psize));
-    } else {
-      t = (int32_t)ceil(__dmul_rn(__dmul_rn(__dmul_rn(tau, tau), (double)psize), 1.0 - 1e-12));
-    }
-    const int mode = (t >= 1 && psize > 0) ? 0 : (psize == 0 && tau > 0.0) ? 1 : 2;
-    if (mode == 0) {
-      if (threadIdx.x < 33) s_hist[threadIdx.x] = 0;
-      __syncthreads();
-      for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
-        const int32_t sg = plist[q];
-        const int64_t len = a.post_ptr[sg + 1] - a.post_ptr[sg];
-        atomicAdd(&s_hist[63 - __clzll((long long)(len > 1 ? len : (int64_t)1))], 1);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int32_t npre = psize - t + 1;
-        int32_t cum = 0, b = 0;
-        for (; b < 33; ++b) {
-          cum += s_hist[b];
-          if (cum >= npre) break;
-        }
-        s_bstar = b;
-      }
-      __syncthreads();
-      const int32_t bstar = s_bstar;
-      for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
-        const int32_t sg = plist[q];
-        const int64_t lo0 = a.post_ptr[sg], hi0 = a.post_ptr[sg + 1];
-        int32_t len_rem = 0, start = 0;
-        if (63 - __clzll((long long)((hi0 - lo0) > 1 ? (hi0 - lo0) : (int64_t)1)) <= bstar) {
-          int64_t lo = lo0, hi = hi0;  // first posting >= pos
-          while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (a.post_item[mid] < pos) lo = mid + 1;
-            else hi = mid;
-          }
-          start = (int32_t)lo;
-          len_rem = (int32_t)(hi0 - lo);
-        }
-        pstart[q] = start;
-        pscan[q] = len_rem;
-      }
-      __syncthreads();
-      const int32_t T = block_exclusive_scan(pscan, psize, s_w, &s_carry);
-      if (threadIdx.x == 0) s_T = T;
-      __syncthreads();
-    } else {
-      __syncthreads();
-    }
-    // ---- enumerate + evaluate; candidates appended (warp-aggregated) to list rid % 3
-    int32_t my_js = INT_MAX;
+    __syncthreads();
+    int mode;
+    int32_t emp_lo;
+    const int64_t total = prepare_round(a, pl, bs, psize, pos, &mode, &emp_lo);
+    int32_t my_js = INT_MAX, my_ok = 0;
     {
       int32_t* cj = a.cand_j + (size_t)slot * m;
       uint8_t* co = a.cand_ok + (size_t)slot * m;
-      int64_t total;
-      if (mode == 0) total = s_T;
-      else if (mode == 1) total = __ldg(a.n_empty);
-      else total = m - pos;
-      int32_t emp_lo = 0;
-      if (mode == 1) {  // first empty item >= pos
-        int32_t lo = 0, hi = __ldg(a.n_empty);
-        while (lo < hi) {
-          const int32_t mid = (lo + hi) >> 1;
-          if (a.empties[mid] < pos) lo = mid + 1;
-          else hi = mid;
-        }
-        emp_lo = lo;
-        total -= lo;
-      }
       for (int64_t e0 = 0; e0 < total; e0 += gthreads) {
         const int64_t e = e0 + gtid;
         bool has = false, ok = false;
         int32_t j = -1;
         if (e < total) {
-          if (mode == 0) {
-            int32_t lo = 0, hi = psize;  // last q with pscan[q] <= e
-            while (hi - lo > 1) {
-              const int32_t mid = (lo + hi) >> 1;
-              if (pscan[mid] <= e) lo = mid;
-              else hi = mid;
-            }
-            j = a.post_item[pstart[lo] + (e - pscan[lo])];
-          } else if (mode == 1) {
-            j = a.empties[emp_lo + e];
-          } else {
-            j = pos + (int32_t)e;
-          }
+          j = entry_item(a, pl, mode, psize, e, pos, emp_lo);
           if (__ldcg(a.group_of_item + j) < 0 && (mode == 2 || atomicExch(a.stamp + j, rid) != rid)) {
             has = true;
-            const int64_t p0 = a.item_ptr[j], p1 = a.item_ptr[j + 1];
-            int64_t inter = 0;
-            for (int64_t p = p0; p < p1; ++p) {
-              const int32_t sg = a.item_seg[p];
-              inter += (sP[sg >> 6] >> (sg & 63)) & 1ull;
-            }
-            const int64_t sz = p1 - p0;
-            ok = accept_dev(inter, psize, sz, tau, a.cosine, a.bounded, cap);
-            if (ok && a.update && inter < sz) my_js = min(my_js, j);
+            bool grows;
+            ok = eval_candidate(a, sP, j, psize, cap, &grows);
+            my_ok += ok ? 1 : 0;
+            if (grows) my_js = min(my_js, j);
           }
         }
         const unsigned act = __activemask();
@@ -975,35 +1192,34 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
         }
       }
     }
-    my_js = __reduce_min_sync(__activemask(), my_js);
-    if (lane == 0 && my_js != INT_MAX) atomicMin(&s_js, my_js);
+    my_js = __reduce_min_sync(0xffffffffu, my_js);
+    my_ok = __reduce_add_sync(0xffffffffu, my_ok);
+    if (lane == 0) {
+      if (my_js != INT_MAX) atomicMin(&s_js, my_js);
+      if (my_ok) atomicAdd(a.ctrl + 10 + slot, my_ok);
+    }
     __syncthreads();
     if (threadIdx.x == 0 && s_js != INT_MAX) atomicMin(a.ctrl + slot, s_js);
     grid_barrier(a.ctrl + 8, a.ctrl + 9);
 
     const int32_t js = *((volatile int32_t*)(a.ctrl + slot));
     const int32_t ccnt = *((volatile int32_t*)(a.ctrl + 3 + slot));
+    const int32_t okcnt = *((volatile int32_t*)(a.ctrl + 10 + slot));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.stats[3] += 1;
+      a.stats[4] += (js >= m && okcnt > 0) ? 1 : 0;
+      a.stats[6] += clock64() - t_phase;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl[(rid + 2) % 3] = INT_MAX;
     if (threadIdx.x == 0) {
       s_rid = rid;
-      s_pending_seed = -1;
       s_acc_list = slot;
       s_acc_cnt = ccnt;
       s_acc_g = g;
+      s_grounds += 1;
     }
     if (js < m) {
-      // ---- growth at js: OR its segments into P (appending new ones to plist in list order)
-      if (threadIdx.x < 32) {
-        const int64_t p0 = a.item_ptr[js], p1 = a.item_ptr[js + 1];
-        int c = 0;
-        for (int64_t p = p0 + lane; p < p1; p += 32) {
-          const int32_t sg = a.item_seg[p];
-          c += (int)((sP[sg >> 6] >> (sg & 63)) & 1ull);
-        }
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (lane == 0) s_inter = c;
-      }
-      __syncthreads();
+      // growth at js: OR its segments into P, appending new ones to the list in list order
       if (threadIdx.x == 0) {
         const int64_t p0 = a.item_ptr[js], p1 = a.item_ptr[js + 1];
         int32_t ps = psize;
@@ -1012,73 +1228,39 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
           const unsigned long long bit = 1ull << (sg & 63);
           if (!(sP[sg >> 6] & bit)) {
             sP[sg >> 6] |= bit;
-            plist[ps++] = sg;
+            pl.seg(ps++) = sg;
           }
         }
-        s_psize = ps;  // = psize + size(js) - inter(js)
+        s_psize = ps;
         s_pos = js + 1;
         s_acc_limit = js;
       }
       __syncthreads();
       continue;
     }
-    // ============================ ACCEPT phase (group complete: all ok candidates of the last round)
-    if (threadIdx.x == 0) s_acc_limit = INT_MAX;
-    __syncthreads();
-    {
+    // group complete: accept the ok candidates of the last round (only if there are any)
+    if (okcnt > 0) {
       const int32_t* cj = a.cand_j + (size_t)slot * m;
       const uint8_t* co = a.cand_ok + (size_t)slot * m;
       for (int64_t i = gtid; i < ccnt; i += gthreads) {
         const int32_t j = __ldcg(cj + i);
         if (__ldcg(co + i)) a.group_of_item[j] = g;
       }
+      grid_barrier(a.ctrl + 8, a.ctrl + 9);
     }
-    grid_barrier(a.ctrl + 8, a.ctrl + 9);
-    // ============================ SEED: first unassigned item after the seed (same in every block)
-    if (threadIdx.x < 32) {
-      int32_t j0 = s_seed + 1;
-      int32_t found = m;
-      for (; j0 < m; j0 += 32) {
-        const int32_t j = j0 + lane;
-        const bool un = j < m && __ldcg(a.group_of_item + j) < 0;
-        const unsigned b = __ballot_sync(0xffffffffu, un);
-        if (b) {
-          found = j0 + __ffs(b) - 1;
-          break;
-        }
-      }
-      if (lane == 0) s_next = found;
-    }
-    __syncthreads();
-    const int32_t nxt = s_next;
-    if (nxt >= m) break;
-    // reset P to the new seed's pattern
-    for (int32_t q = threadIdx.x; q < psize; q += blockDim.x) {
-      const int32_t sg = plist[q];
-      atomicAnd(&sP[sg >> 6], ~(1ull << (sg & 63)));
-    }
-    __syncthreads();
-    {
-      const int64_t p0 = a.item_ptr[nxt], len = a.item_ptr[nxt + 1] - p0;
-      for (int64_t k = threadIdx.x; k < len; k += blockDim.x) {
-        const int32_t sg = a.item_seg[p0 + k];
-        plist[k] = sg;
-        atomicOr(&sP[sg >> 6], 1ull << (sg & 63));
-      }
-      if (threadIdx.x == 0) {
-        s_psize = (int32_t)len;
-        s_cap = __ddiv_rn((double)len, cap_den);
-        s_pos = nxt + 1;
-        s_seed = nxt;
-        s_g = g + 1;
-        s_acc_cnt = 0;
-        s_pending_seed = nxt;  // written after the next barrier (other CTAs may still be scanning)
-        if (blockIdx.x == 0) a.seed_item[g + 1] = nxt;
+    if (threadIdx.x == 0) {
+      s_acc_cnt = 0;
+      // a singleton group (one round, nothing accepted) leaves the batch's later verdicts valid
+      if (s_grounds == 1 && okcnt == 0 && s_bpos < s_blen) {
+        s_mode = 2;
+      } else {
+        s_mode = 0;
+        s_next = s_seed + 1;
       }
     }
     __syncthreads();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl[6] = s_g + 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl[6] = s_gnext;
 }
 
 // patterns of the sparse path: unique (group, segment) pairs of all member items
@@ -1179,10 +1361,9 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
   RB_CUDA_TRY(cudaGetLastError());
   // ---- K3: pruned greedy scan
   {
-    int32_t ctrl0[32];
-    for (int i = 0; i < 32; ++i) ctrl0[i] = 0;
+    std::vector<int32_t> ctrl0(16 + 2 * kSparseBlocks, 0);
     for (int i = 0; i < 3; ++i) ctrl0[i] = INT_MAX;
-    RB_CUDA_TRY(cudaMemcpyAsync(ws.ctrl, ctrl0, sizeof(ctrl0), cudaMemcpyHostToDevice, stream));
+    RB_CUDA_TRY(cudaMemcpyAsync(ws.ctrl, ctrl0.data(), sizeof(int32_t) * ctrl0.size(), cudaMemcpyHostToDevice, stream));
     SGreedyArgs ga;
     ga.m = m;
     ga.n_seg = (int32_t)n_seg;
@@ -1205,7 +1386,9 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     ga.seed_item = ws.seed_item;
     ga.ctrl = ws.ctrl;
     ga.scratch = ws.scratch;
-    const size_t shm = sizeof(uint64_t) * W;
+    ga.stats = ws.stats;
+    RB_CUDA_TRY(cudaMemsetAsync(ws.stats, 0, 8 * 8, stream));
+    const size_t shm = sizeof(uint64_t) * W + sizeof(int32_t) * 3 * kPlistSmem;
     if (shm > 200 * 1024) return fail(RB_EUNSUPPORTED, "too many segments for the pattern bitset in shared memory");
     void* fn = (void*)sparse_greedy_kernel;
     if (shm > 48 * 1024) RB_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -1218,6 +1401,7 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
       if (per_sm < 1) return fail(RB_ECUDA, "sparse greedy kernel cannot be resident");
       blocks = std::min(sms, kSparseBlocks);
     }
+    if (const char* b = std::getenv("RB_1SA_BLOCKS")) blocks = std::max(1, std::min(std::atoi(b), kSparseBlocks));
     void* args[] = {&ga};
     RB_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kSparseThreads), args, shm, stream));
   }
@@ -1225,6 +1409,13 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
   RB_CUDA_TRY(cudaMemcpyAsync(&H32, ws.ctrl + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
   RB_CUDA_TRY(cudaStreamSynchronize(stream));
   const int64_t H = H32;
+  if (std::getenv("RB_1SA_STATS")) {
+    unsigned long long st[8];
+    RB_CUDA_TRY(cudaMemcpy(st, ws.stats, sizeof(st), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[rb 1sa sparse] m=%d H=%lld batches=%llu seeds=%llu singletons=%llu rounds=%llu accepts=%llu "
+            "batch_Mcyc=%.1f group_Mcyc=%.1f\n", m, (long long)H, st[0], st[1], st[2], st[3], st[4], st[5] / 1e6,
+            st[6] / 1e6);
+  }
   // ---- assembly (as the dense path)
   assembly_keys_kernel<<<g1, 256, 0, stream>>>(ws.item_of_row, ws.group_of_item, n, m, ws.keys_a, ws.vals_a);
   {
