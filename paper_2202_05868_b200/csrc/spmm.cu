@@ -71,7 +71,16 @@ struct SpmmArgs {
   uint32_t ab_fmt;      // 0 = f16, 1 = bf16
   uint32_t a_evict_first;  // L2 policy of A-tile loads: 1 = evict_first, 0 = evict_normal
   int32_t short_ns;        // C columns per short item: 128 or 256
+  float* ws;               // split-K partials of tall units: [slot][split][8 warps][8 chunks][32 cols][32 lanes]
+  int32_t* cnt;            // split-K arrival counters: [slot][8 warps] (zero between launches)
 };
+
+// Tall work unit = two int4: (g, m, n0, k0) and (k1, split, n_splits, slot).  Units with
+// n_splits > 1 cover the K range [k0, k1) of a split item; their partial accumulators meet in
+// `ws` ([slot][split][warp][chunk][8][lane] float4), and the epilogue warp that arrives last
+// sums them in split order (deterministic: the sum order does not depend on arrival order).
+constexpr int MAX_SPLIT = 4;
+constexpr int WARP_PART = 8 * 32 * 32;  // floats of one epilogue warp's partial (32 rows x 256 cols)
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -154,14 +163,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const uint64_t pol_b = policy_evict_last();
       PipeState ps;
       for (int i = pair; i < a.n_items; i += n_pairs) {
-        const int4 it = a.items[i];
+        const int4 it = a.items[2 * i], iu = a.items[2 * i + 1];
         const int g = it.x, m = it.y, n0 = it.z;
         const int h = a.row_partition[g + 1] - a.row_partition[g];
         const int hp = hp_of(h);
         const int b_begin = a.blk_ptr[g];
-        const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
         const int64_t row0 = a.grp_tile_row[g] + (int64_t)m * PAIR_BM + rank * 128;
-        for (int k = 0; k < nk; ++k) {
+        for (int k = it.w; k < iu.x; ++k) {
           mbar_wait(&empty[ps.s], ps.ph ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[ps.s], 2 * T_STAGE);
           const int t = k / a.dp_chunks, kc = k - t * a.dp_chunks;
@@ -190,13 +198,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int acc = 0;
       uint32_t aph = 0;
       for (int i = pair; i < a.n_items; i += n_pairs) {
-        const int g = a.items[i].x;
-        const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
-        if (nk == 0) continue;
+        const int k0 = a.items[2 * i].w, k1 = a.items[2 * i + 1].x;
+        if (k1 <= k0) continue;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
-        for (int k = 0; k < nk; ++k) {
+        for (int k = k0; k < k1; ++k) {
           mbar_wait(&full[ps.s], ps.ph);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + ps.s * T_STAGE);
@@ -205,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           for (int kk = 0; kk < KCH / 16; ++kk) {
             const uint64_t ad = sdesc_sw128(a_base + kk * 32, 16, 1024);            // K-major: +16 elems
             const uint64_t bd = sdesc_sw128(b_base + kk * 2048, BOX_BYTES, 1024);   // MN-major: +16 rows
-            umma_f16_2sm(d, ad, bd, idesc, (k | kk) != 0);
+            umma_f16_2sm(d, ad, bd, idesc, (k != k0) || kk != 0);
           }
           umma_commit_2sm_mc(&empty[ps.s], 0x3);
           ps.advance(T_STAGES);
@@ -222,11 +229,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     int acc = 0;
     uint32_t aph = 0;
     for (int i = pair; i < a.n_items; i += n_pairs) {
-      const int4 it = a.items[i];
+      const int4 it = a.items[2 * i], iu = a.items[2 * i + 1];
       const int g = it.x, m = it.y, n0 = it.z;
       const int p0 = a.row_partition[g];
       const int h = a.row_partition[g + 1] - p0;
-      const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
+      const int nk = iu.x - it.w;
       const int row_local = m * PAIR_BM + (int)rank * 128 + q * 32 + lane;
       const bool valid = row_local < h;
       const int64_t crow = valid ? (int64_t)a.row_perm[p0 + row_local] : 0;
@@ -235,6 +242,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       if (nk > 0) {
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
+      }
+      if (iu.z > 1) {
+        // split-K unit: park the partial (lane-contiguous, coalesced), release the accumulator,
+        // and let the last-arriving split of this warp's 32 rows reduce all partials in split order
+        const int wslot = (int)rank * 4 + q;
+        float* part = a.ws + ((size_t)iu.w * MAX_SPLIT + iu.y) * 8 * WARP_PART + (size_t)wslot * WARP_PART;
+        float4* part4 = reinterpret_cast<float4*>(part);
+        for (int c = 0; c < ncol; c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16) + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)  // [chunk][j][lane] float4: 512 contiguous bytes per instruction
+            __stcg(part4 + (c >> 5) * 256 + j * 32 + lane,
+                   make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+        __threadfence();
+        __syncwarp();
+        int old = 0;
+        int* ctr = a.cnt + iu.w * 8 + wslot;
+        if (lane == 0) old = atomicAdd(ctr, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == iu.z - 1) {
+          __threadfence();
+          const float4* base4 =
+              reinterpret_cast<const float4*>(a.ws + (size_t)iu.w * MAX_SPLIT * 8 * WARP_PART + (size_t)wslot * WARP_PART);
+          constexpr int SPLIT_STRIDE4 = 8 * WARP_PART / 4;
+          for (int c = 0; c < ncol; c += 32) {
+            // all splits' loads of this chunk in flight at once, then summed in split order
+            float4 v[MAX_SPLIT][8];
+#pragma unroll
+            for (int sp = 0; sp < MAX_SPLIT; ++sp)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                v[sp][j] = sp < iu.z ? __ldcg(base4 + sp * SPLIT_STRIDE4 + (c >> 5) * 256 + j * 32 + lane)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t r[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 t = v[0][j];
+#pragma unroll
+              for (int sp = 1; sp < MAX_SPLIT; ++sp)
+                if (sp < iu.z) {
+                  t.x += v[sp][j].x;
+                  t.y += v[sp][j].y;
+                  t.z += v[sp][j].z;
+                  t.w += v[sp][j].w;
+                }
+              r[4 * j] = __float_as_uint(t.x);
+              r[4 * j + 1] = __float_as_uint(t.y);
+              r[4 * j + 2] = __float_as_uint(t.z);
+              r[4 * j + 3] = __float_as_uint(t.w);
+            }
+            if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+          }
+          if (lane == 0) *ctr = 0;  // ready for the next launch (stream ordered)
+        }
+        continue;
       }
       for (int c = 0; c < ncol; c += 32) {
         uint32_t r[32];
@@ -546,7 +617,10 @@ struct rb_spmm_plan {
   rb_vbr_device v;
   int64_t N;
   int32_t b_dtype;
-  int4* d_items = nullptr;  // tall items, then short items, then simt items
+  int4* d_items = nullptr;  // tall units (2 x int4 each), then short items, then simt items
+  float* d_ws = nullptr;    // split-K partials of the tall tail
+  int32_t* d_cnt = nullptr;
+  int64_t n_split_slots = 0;
   int32_t short_ns = rb::SHORT_NS;
   int64_t n_tall = 0, n_short = 0, n_simt = 0;
   CUtensorMap tmA16, tmA32, tmA64, tmA128;
@@ -554,6 +628,68 @@ struct rb_spmm_plan {
 };
 
 using namespace rb;
+
+namespace {
+
+// Static round-robin makespan (the persistent kernel hands unit i to pair i % P) in K steps; each
+// split unit pays `split_cost` extra steps for parking and re-reading its partial.
+double rr_makespan(const std::vector<int>& len, const std::vector<int>& nsplit, int P, double split_cost) {
+  std::vector<double> t(P, 0.0);
+  for (size_t i = 0; i < len.size(); ++i) t[i % P] += len[i] + (nsplit[i] > 1 ? split_cost : 0.0);
+  return *std::max_element(t.begin(), t.end());
+}
+
+// Tall items (g, m, n0, L = K steps), LPT-sorted, become units.  The last partial wave is the
+// tail: keep every full wave whole and split each tail item into s equal K ranges so the tail
+// fits one wave (r*s <= P), choosing the s with the smallest static makespan.  Measured on B200
+// (tools/split_probe.py): the partial park + reduce costs far more than its bytes suggest when
+// units get short, so units stay >= 128 K steps and a split must win by > 5 %: config 2
+// (tail 34/74 pairs, L = 512) splits in two (0.674 -> 0.650 ms); config 4 (tail 54/74) does not.
+// A split item's units are adjacent so they run concurrently on neighbouring pairs.
+void split_tail(const std::vector<int4>& items, int P, std::vector<int4>& units, int64_t& n_slots) {
+  const int n = (int)items.size();
+  const int full = P > 0 ? n / P : n;
+  int best_s = 1;
+  const char* env = std::getenv("RB_TALL_SPLIT");
+  const int max_s = env ? std::max(1, std::min(MAX_SPLIT, std::atoi(env))) : MAX_SPLIT;
+  const int r = n - full * P;
+  if (P > 0 && r > 0 && max_s > 1) {
+    auto eval = [&](int s) {
+      std::vector<int> len, ns;
+      for (int i = 0; i < n; ++i) {
+        const int L = items[i].w;
+        const int si = (i >= full * P && L >= 128 * s) ? s : 1;
+        for (int j = 0; j < si; ++j) {
+          len.push_back(L * (j + 1) / si - L * j / si);
+          ns.push_back(si);
+        }
+      }
+      return rr_makespan(len, ns, P, 8.0);
+    };
+    double best = eval(1);
+    for (int s = 2; s <= max_s && r * s <= P; ++s) {
+      const double t = eval(s);
+      if (t < best * 0.95) {
+        best = t;
+        best_s = s;
+      }
+    }
+  }
+  const int best_f = full;
+  n_slots = 0;
+  for (int i = 0; i < n; ++i) {
+    const int4 it = items[i];
+    const int L = it.w;
+    const int si = (i >= best_f * P && best_s > 1 && L >= 128 * best_s) ? best_s : 1;
+    const int slot = si > 1 ? (int)n_slots++ : -1;
+    for (int j = 0; j < si; ++j) {
+      units.push_back(make_int4(it.x, it.y, it.z, L * j / si));
+      units.push_back(make_int4(L * (j + 1) / si, j, si, slot));
+    }
+  }
+}
+
+}  // namespace
 
 extern "C" int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* blk_ptr, int64_t n_block_rows,
                                    int32_t b_dtype, int32_t dp, int32_t shard, int32_t n_shards, int64_t* row_begin,
@@ -617,7 +753,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
     } else {
       for (int m = 0; m < (h + PAIR_BM - 1) / PAIR_BM; ++m) {
         if (rp[g] + m * PAIR_BM < row_lo || rp[g] + m * PAIR_BM >= row_hi) continue;
-        for (int64_t n0 = 0; n0 < N; n0 += TALL_BN) tall.push_back(make_int4((int)g, m, (int)n0, nb));
+        for (int64_t n0 = 0; n0 < N; n0 += TALL_BN) tall.push_back(make_int4((int)g, m, (int)n0, nb * dpc));
         exec_flops += 2.0 * nb * dpc * KCH * PAIR_BM * (double)((N + TALL_BN - 1) / TALL_BN * TALL_BN);
         vbr_flops += 2.0 * nb * std::min(PAIR_BM, h - m * PAIR_BM) * (double)vbr->dp * N;
       }
@@ -634,32 +770,47 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   // Longest-first (LPT against the tail) for the tall items, stable so the N chunks of one pair tile
   // stay adjacent (they run concurrently and share the A tile through L2).
   std::stable_sort(tall.begin(), tall.end(), [](const int4& x, const int4& y) { return x.w > y.w; });
+  int dev = 0, sms = kNumSMs;
+  RB_CUDA_TRY(cudaGetDevice(&dev));
+  RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::vector<int4> tall_units;
+  int64_t n_slots = 0;
+  split_tail(tall, sms / 2, tall_units, n_slots);
 
   auto* p = new rb_spmm_plan();
   p->v = *vbr;
   p->N = N;
   p->b_dtype = b_dtype;
   p->short_ns = short_ns;
-  p->n_tall = (int64_t)tall.size();
+  p->n_tall = (int64_t)tall_units.size() / 2;
+  p->n_split_slots = n_slots;
   p->n_short = (int64_t)shrt.size();
   p->n_simt = (int64_t)simt.size();
-  const int64_t n_items = p->n_tall + p->n_short + p->n_simt;
+  const int64_t n_items = 2 * p->n_tall + p->n_short + p->n_simt;
+  if (n_slots > 0) {
+    cudaError_t e = cudaMalloc(&p->d_ws, sizeof(float) * (size_t)n_slots * MAX_SPLIT * 8 * WARP_PART);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_cnt, sizeof(int32_t) * 8 * n_slots);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_cnt, 0, sizeof(int32_t) * 8 * n_slots, stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(RB_ENOMEM, "cudaMalloc split-K workspace");
+    }
+  }
   if (n_items > 0) {
     cudaError_t e = cudaMalloc(&p->d_items, sizeof(int4) * n_items);
     if (e != cudaSuccess) {
-      delete p;
+      rb_spmm_plan_destroy(p);
       return fail(RB_ENOMEM, "cudaMalloc work list");
     }
     std::vector<int4> all;
     all.reserve(n_items);
-    all.insert(all.end(), tall.begin(), tall.end());
+    all.insert(all.end(), tall_units.begin(), tall_units.end());
     all.insert(all.end(), shrt.begin(), shrt.end());
     all.insert(all.end(), simt.begin(), simt.end());
     e = cudaMemcpyAsync(p->d_items, all.data(), sizeof(int4) * n_items, cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) {
-      cudaFree(p->d_items);
-      delete p;
+      rb_spmm_plan_destroy(p);
       return fail(RB_ECUDA, cudaGetErrorString(e));
     }
   }
@@ -698,6 +849,8 @@ extern "C" int rb_spmm_plan_info(const rb_spmm_plan* p, rb_spmm_info* info) {
 extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (!p) return RB_OK;
   if (p->d_items) cudaFree(p->d_items);
+  if (p->d_ws) cudaFree(p->d_ws);
+  if (p->d_cnt) cudaFree(p->d_cnt);
   delete p;
   return RB_OK;
 }
@@ -722,9 +875,11 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.ab_fmt = p->b_dtype == RB_BF16 ? 1u : 0u;
   a.a_evict_first = 0;
   a.short_ns = p->short_ns;
+  a.ws = p->d_ws;
+  a.cnt = p->d_cnt;
   if (p->b_dtype == RB_F32) {
     if (p->n_simt > 0) {
-      a.items = p->d_items;
+      a.items = p->d_items + 2 * p->n_tall + p->n_short;
       a.n_items = (int32_t)p->n_simt;
       a.dp_chunks = 1;
       spmm_simt_f32_kernel<<<(unsigned)p->n_simt, SIMT_COLS, 0, stream>>>(
@@ -758,7 +913,7 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
     RB_CUDA_TRY(cudaGetLastError());
   }
   if (p->n_short > 0) {
-    a.items = p->d_items + p->n_tall;
+    a.items = p->d_items + 2 * p->n_tall;
     a.n_items = (int32_t)p->n_short;
     a.a_evict_first = 1;
     const int ctas = (int)std::min<int64_t>(sms, p->n_short);

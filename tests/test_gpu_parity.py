@@ -250,3 +250,45 @@ def test_block_1sa_sparse_path_medium(name, force_sparse_1sa):
     case = load_golden(name)
     g = rb.block_1sa(csr_of(case), part_of(case), policy_of(case), bool(case["use_compression"]))
     check_grouping(g, case, name)
+
+
+@pytest.mark.parametrize("split", ["2", "1"])
+def test_spmm_tall_split_k_tail(split, monkeypatch):
+    """Tall block rows whose last wave is split along K (partials reduced by the last-arriving
+    epilogue warp, in split order): C within the bf16 tolerance, bit-identical run to run (the
+    arrival counters reset themselves), and RB_TALL_SPLIT=1 (no split) agrees to tolerance."""
+    from paper_2202_05868_b200.device import DeviceCsr, DeviceVbr
+    from paper_2202_05868_b200.types import csr_from_coo
+
+    monkeypatch.setenv("RB_TALL_SPLIT", split)
+    rng = np.random.default_rng(11)
+    heights = [300, 257, 520]  # 2 + 2 + 3 pair tiles (256 rows each)
+    n_cols, delta, N = 16384, 64, 300  # 256 segments -> 256 K steps per item; 2 N chunks (second ragged)
+    rows, cols, r0 = [], [], 0
+    for h in heights:
+        nnz = h * 40
+        rows.append(r0 + rng.integers(0, h, nnz))
+        cols.append(rng.integers(0, n_cols, nnz))
+        r0 += h
+    keys = np.unique(np.concatenate(rows) * n_cols + np.concatenate(cols))
+    vals = rounded(rng.uniform(0.1, 1.0, len(keys)), torch.bfloat16) * rng.choice([-1.0, 1.0], len(keys))
+    A = csr_from_coo(r0, n_cols, keys // n_cols, keys % n_cols, vals)
+    perm = torch.from_numpy(rng.permutation(r0)).cuda()
+    rp = torch.tensor(np.concatenate([[0], np.cumsum(heights)]), device="cuda")
+    q = rb.ColumnPartition.uniform(n_cols, delta)
+    dv = DeviceVbr.build(DeviceCsr.from_host(A, "cuda"), q, perm, rp, dtypes=("bf16",))
+    info = dv.plan_info(N, "bf16")
+    n_items = (2 + 2 + 3) * 2
+    if split == "1":
+        assert info["n_items_tall"] == n_items
+    else:
+        assert info["n_items_tall"] > n_items  # the tail was split
+    B = rounded(rng.uniform(-1, 1, (n_cols, N)), torch.bfloat16)
+    Bd = torch.zeros((n_cols, 304), dtype=torch.bfloat16, device="cuda")[:, :N]  # 16-byte row stride
+    Bd.copy_(torch.from_numpy(B))
+    C1 = dv.spmm(Bd)
+    C2 = dv.spmm(Bd)
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)
+    Ad = A.to_dense()
+    assert_close(C1.cpu().numpy().astype(np.float64), Ad @ B, np.abs(Ad) @ np.abs(B), 1e-4, f"split={split}")
