@@ -269,7 +269,7 @@ def run_ours(args, world, rank):
     N = cfg.N
     C = torch.empty((dA.n_rows, N), dtype=torch.float32, device=device)
     info = dv.plan_info(N, prec, rank, world)
-    launches_per_step = int(info["n_items_tall"] > 0) + int(info["n_items_short"] > 0) + int(info["n_items_simt"] > 0)
+    launches_per_step = int(info["n_launches"])
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):

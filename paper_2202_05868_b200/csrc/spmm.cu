@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "spmm_skinny.cuh"
 
 namespace rb {
 
@@ -623,6 +624,11 @@ struct rb_spmm_plan {
   int64_t n_split_slots = 0;
   int32_t short_ns = rb::SHORT_NS;
   int64_t n_tall = 0, n_short = 0, n_simt = 0;
+  rb::SkinnyItem* d_skinny = nullptr;  // skinny items, grouped by height class
+  float* d_skinny_ws = nullptr;     // partials of split skinny block rows
+  int32_t* d_skinny_cnt = nullptr;
+  unsigned long long* d_sched = nullptr;  // 2 work counters per skinny height class
+  int64_t skinny_off[rb::SKINNY_CLASSES + 1] = {0, 0, 0, 0, 0};
   CUtensorMap tmA16, tmA32, tmA64, tmA128;
   rb_spmm_info info;
 };
@@ -734,12 +740,23 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   // slower, so 256 is the default.  RB_SHORT_NS=128 overrides.
   int32_t short_ns = rb::SHORT_NS;
   if (const char* ns_env = std::getenv("RB_SHORT_NS")) short_ns = std::atoi(ns_env) >= 256 ? 256 : 128;
+  // block rows with h <= skinny_h run on the CUDA cores (spmm_skinny.cu): a tensor-core tile would
+  // be >= 15/16 padding rows.  fp32 path: h <= 8; tensor path: h <= 4 (RB_SKINNY_H overrides, 0..8).
+  int skinny_h = tc ? 4 : 8;
+  if (const char* sk = std::getenv("RB_SKINNY_H")) skinny_h = std::max(0, std::min(8, std::atoi(sk)));
+  const int sk_cols = skinny_cols(b_dtype, N);
+  std::vector<SkinnyItem> skinny[SKINNY_CLASSES];
+  int64_t sk_slots = 0, sk_units = 0;
   std::vector<int32_t> short_rows;
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
     if (h <= 0 || rp[g + 1] <= row_lo || rp[g] >= row_hi) continue;
-    if (!tc) {
+    if (h <= skinny_h) {
+      skinny_items_for_row((int32_t)g, h, bp[g], nb, N, sk_cols, skinny[skinny_class(h)], sk_slots, sk_units);
+      exec_flops += 2.0 * nb * h * (double)vbr->dp * N;
+      vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
+    } else if (!tc) {
       for (int r0 = 0; r0 < h; r0 += SIMT_ROWS) {
         if (rp[g] + r0 < row_lo || rp[g] + r0 >= row_hi) continue;
         for (int64_t n0 = 0; n0 < N; n0 += SIMT_COLS) simt.push_back(make_int4((int)g, r0, (int)n0, nb));
@@ -786,6 +803,29 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   p->n_split_slots = n_slots;
   p->n_short = (int64_t)shrt.size();
   p->n_simt = (int64_t)simt.size();
+  // longest first: groups pull items dynamically, so LPT order keeps the tail short
+  for (int c = 0; c < SKINNY_CLASSES; ++c)
+    std::stable_sort(skinny[c].begin(), skinny[c].end(),
+                     [](const SkinnyItem& x, const SkinnyItem& y) { return x.be - x.bb > y.be - y.bb; });
+  for (int c = 0; c < SKINNY_CLASSES; ++c) p->skinny_off[c + 1] = p->skinny_off[c] + (int64_t)skinny[c].size();
+  if (p->skinny_off[SKINNY_CLASSES] > 0) {
+    std::vector<SkinnyItem> all;
+    all.reserve(p->skinny_off[SKINNY_CLASSES]);
+    for (int c = 0; c < SKINNY_CLASSES; ++c) all.insert(all.end(), skinny[c].begin(), skinny[c].end());
+    cudaError_t e = cudaMalloc(&p->d_skinny, sizeof(SkinnyItem) * all.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_sched, sizeof(unsigned long long) * 2 * SKINNY_CLASSES);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_sched, 0, sizeof(unsigned long long) * 2 * SKINNY_CLASSES, stream);
+    if (e == cudaSuccess && sk_slots > 0) e = cudaMalloc(&p->d_skinny_ws, sizeof(float) * 128 * (size_t)sk_units);
+    if (e == cudaSuccess && sk_slots > 0) e = cudaMalloc(&p->d_skinny_cnt, sizeof(int32_t) * (size_t)sk_slots);
+    if (e == cudaSuccess && sk_slots > 0) e = cudaMemsetAsync(p->d_skinny_cnt, 0, sizeof(int32_t) * sk_slots, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_skinny, all.data(), sizeof(SkinnyItem) * all.size(), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "skinny work list");
+    }
+  }
   const int64_t n_items = 2 * p->n_tall + p->n_short + p->n_simt;
   if (n_slots > 0) {
     cudaError_t e = cudaMalloc(&p->d_ws, sizeof(float) * (size_t)n_slots * MAX_SPLIT * 8 * WARP_PART);
@@ -833,6 +873,9 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   p->info.n_items_tall = p->n_tall;
   p->info.n_items_short = p->n_short;
   p->info.n_items_simt = p->n_simt;
+  p->info.n_items_skinny = p->skinny_off[SKINNY_CLASSES];
+  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0);
+  for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   p->info.executed_flops = exec_flops;
   p->info.vbr_flops = vbr_flops;
   p->info.row_begin_perm = row_lo < row_hi ? row_lo : -1;
@@ -851,6 +894,10 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_items) cudaFree(p->d_items);
   if (p->d_ws) cudaFree(p->d_ws);
   if (p->d_cnt) cudaFree(p->d_cnt);
+  if (p->d_skinny) cudaFree(p->d_skinny);
+  if (p->d_skinny_ws) cudaFree(p->d_skinny_ws);
+  if (p->d_skinny_cnt) cudaFree(p->d_skinny_cnt);
+  if (p->d_sched) cudaFree(p->d_sched);
   delete p;
   return RB_OK;
 }
@@ -877,6 +924,30 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.short_ns = p->short_ns;
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
+  if (p->skinny_off[SKINNY_CLASSES] > 0) {
+    SkinnyArgs k;
+    k.row_partition = p->v.row_partition;
+    k.row_perm = p->v.row_perm;
+    k.blk_ptr = p->v.blk_ptr;
+    k.blk_col = p->v.blk_col;
+    k.grp_tile_row = p->v.grp_tile_row;
+    k.col_bounds = p->v.col_bounds;
+    k.tiles = p->v.tiles;
+    k.dp = p->v.dp;
+    k.B = B;
+    k.ldb = ldb;
+    k.C = C;
+    k.ldc = ldc;
+    k.N = (int32_t)p->N;
+    k.ws = p->d_skinny_ws;
+    k.cnt = p->d_skinny_cnt;
+    for (int c = 0; c < SKINNY_CLASSES; ++c) {
+      k.items = p->d_skinny + p->skinny_off[c];
+      k.n_items = p->skinny_off[c + 1] - p->skinny_off[c];
+      int rc = launch_skinny(k, p->b_dtype, c, p->d_sched + 2 * c, stream);
+      if (rc) return rc;
+    }
+  }
   if (p->b_dtype == RB_F32) {
     if (p->n_simt > 0) {
       a.items = p->d_items + 2 * p->n_tall + p->n_short;

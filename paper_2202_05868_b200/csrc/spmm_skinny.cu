@@ -1,0 +1,515 @@
+// Skinny block rows (h <= 8) of the VBR SpMM on the CUDA cores (replaces spmm_vbr's per-block
+// `data @ B[bounds]` for the block rows where a tensor-core tile would be >= 94 % padding,
+// multiply.py:84-89).
+//
+// 1-SA leaves most rows of sparse inputs (configs 1, 2b, 3) in block rows of one or two rows: an
+// MMA tile of 16 x 64 would then multiply >= 15 padding rows and every zero column of the tile,
+// and fetch the whole 64-row B panel per block.  Here a lane group (32 lanes, or 16 when N <= 128)
+// owns one block row (or one part of a long one) and a slab of C columns (16-byte B loads per
+// lane), reads the stored tiles and gathers only the B rows of tile columns that hold a nonzero.
+// Groups pull items from a self-resetting work counter (persistent grid), items are ordered
+// longest first, and block rows with > 256 stored blocks are cut into parts whose partials are
+// summed in part order by the last-arriving part.
+//
+// Accumulation order per C element is fixed — blocks ascending, k ascending (parts in order) — so
+// C is deterministic, and on the fp32 path identical to the dense-tile order (skipped terms are
+// exact zeros: fma(0, b, acc) == acc for finite b).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "spmm_skinny.cuh"
+
+namespace rb {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+template <>
+__device__ __forceinline__ float to_f<__half>(__half x) {
+  return __half2float(x);
+}
+template <>
+__device__ __forceinline__ float to_f<float>(float x) {
+  return x;
+}
+
+// 16 bytes of one B row (VEC = 16 / sizeof(T) elements from column n), kept raw until the FMA so
+// eight gathers in flight cost 32 registers.  Columns >= N read as 0.
+template <typename T, bool ALIGNED>
+__device__ __forceinline__ uint4 load_b_raw(const T* p, int n, int N) {
+  constexpr int VEC = 16 / sizeof(T);
+  if (ALIGNED && n + VEC <= N) return __ldg(reinterpret_cast<const uint4*>(p));
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (n + e < N) w[e] = __float_as_uint(__ldg(reinterpret_cast<const float*>(p) + e));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (n + e < N) w[e >> 1] |= (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p) + e) << (16 * (e & 1));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <typename T>
+__device__ __forceinline__ float elem(const uint4& u, int e) {
+  if constexpr (sizeof(T) == 4) {
+    return __uint_as_float(e == 0 ? u.x : e == 1 ? u.y : e == 2 ? u.z : u.w);
+  } else {
+    const uint32_t x = (e >> 1) == 0 ? u.x : (e >> 1) == 1 ? u.y : (e >> 1) == 2 ? u.z : u.w;
+    const uint16_t b = (uint16_t)((e & 1) ? (x >> 16) : (x & 0xffffu));
+    T t;
+    memcpy(&t, &b, 2);
+    return to_f(t);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void fma_row(float (&acc)[16 / sizeof(T)], float a, const uint4& u) {
+#pragma unroll
+  for (int e = 0; e < (int)(16 / sizeof(T)); ++e) acc[e] = __fmaf_rn(a, elem<T>(u, e), acc[e]);
+}
+
+template <int VEC, bool ALIGNED>
+__device__ __forceinline__ void store_c(float* dst, int n, int N, const float (&v)[VEC]) {
+  if (ALIGNED && n + VEC <= N) {
+#pragma unroll
+    for (int e = 0; e < VEC; e += 4)
+      *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      if (n + e < N) dst[e] = v[e];
+  }
+}
+
+// Epilogue shared by both kernels: direct store, or (split block row) park the partial and let the
+// last-arriving part sum every part's partial in part order.
+template <int H, int VEC, int LPR, bool ALIGNED>
+__device__ __forceinline__ void skinny_finish(const SkinnyArgs& a, const SkinnyItem& it, int cols, int h, int p0,
+                                              int n, int gl, unsigned gmask, float (&acc)[H][VEC]) {
+  if (it.nparts > 1) {
+    float* mine = a.ws + ((size_t)it.wsoff + (size_t)it.part * H * (cols / 128)) * 128;
+#pragma unroll
+    for (int r = 0; r < H; ++r)
+#pragma unroll
+      for (int e = 0; e < VEC; e += 4)
+        __stcg(reinterpret_cast<float4*>(mine + r * cols + gl * VEC + e),
+               make_float4(acc[r][e], acc[r][e + 1], acc[r][e + 2], acc[r][e + 3]));
+    __threadfence();
+    __syncwarp(gmask);
+    int old = 0;
+    if (gl == 0) old = atomicAdd(a.cnt + it.slot, 1);
+    old = __shfl_sync(gmask, old, 0, LPR);
+    if (old != it.nparts - 1) return;
+    __threadfence();
+    const float* base = a.ws + (size_t)it.wsoff * 128 + gl * VEC;
+    const size_t pstride = (size_t)H * cols;
+#pragma unroll
+    for (int r = 0; r < H; ++r)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[r][e] = 0.f;
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      for (int q = 0; q < it.nparts; q += 4) {  // four parts' loads in flight, summed in part order
+        float4 v[4][VEC / 4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q + u < it.nparts)
+#pragma unroll
+            for (int e = 0; e < VEC / 4; ++e)
+              v[u][e] = __ldcg(reinterpret_cast<const float4*>(base + (q + u) * pstride + r * cols) + e);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q + u < it.nparts)
+#pragma unroll
+            for (int e = 0; e < VEC / 4; ++e) {
+              acc[r][4 * e] += v[u][e].x;
+              acc[r][4 * e + 1] += v[u][e].y;
+              acc[r][4 * e + 2] += v[u][e].z;
+              acc[r][4 * e + 3] += v[u][e].w;
+            }
+      }
+    }
+    if (gl == 0) a.cnt[it.slot] = 0;  // ready for the next launch (stream ordered)
+  }
+  if (n >= a.N) return;
+#pragma unroll
+  for (int r = 0; r < H; ++r)
+    if (r < h) store_c<VEC, ALIGNED>(a.C + (int64_t)a.row_perm[p0 + r] * a.ldc + n, n, a.N, acc[r]);
+}
+
+__device__ __forceinline__ SkinnyItem load_item(const SkinnyItem* p) {
+  const int4 x = __ldg(reinterpret_cast<const int4*>(p)), y = __ldg(reinterpret_cast<const int4*>(p) + 1);
+  return SkinnyItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+}
+
+// Persistent scheduling: lane 0 of a group pulls the next item index; every group overshoots the
+// counter exactly once, and the last group to leave resets both counters for the next launch.
+template <int LPR>
+__device__ __forceinline__ int64_t next_item(unsigned long long* sched, int gl, unsigned gmask) {
+  unsigned long long i = 0;
+  if (gl == 0) i = atomicAdd(sched, 1ull);
+  return (int64_t)__shfl_sync(gmask, i, 0, LPR);
+}
+template <int LPR>
+__device__ __forceinline__ void leave(unsigned long long* sched, int gl, unsigned long long total_groups) {
+  if (gl == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1ull) == total_groups - 1) {
+      sched[0] = 0ull;
+      sched[1] = 0ull;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// h == 1 (the common case on sparse inputs), tiles at most 64 columns wide.  Per batch of LPR
+// blocks the lane group
+//   * stages the blocks' tile rows in shared memory with cp.async (double buffered: the next
+//     batch's rows and block columns are in flight while this batch's B rows are gathered),
+//   * lane j turns staged row j into a 64-bit nonzero mask (16-byte shared loads, padded rows),
+//   * a group prefix sum orders the nonzeros (block ascending, k ascending) into a list,
+//   * the list is streamed with eight B-row gathers in flight per lane.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <typename T, int LPR>
+struct Skinny1Smem {
+  static constexpr int KC = 64;                          // tile columns staged per block (dp <= 64)
+  static constexpr int PPB = KC * (int)sizeof(T) / 16;   // 16-byte pieces per staged row
+  static constexpr int ROW = KC * (int)sizeof(T) + 16;   // padded row stride: conflict-free row reads
+  static constexpr int STAGE = LPR * ROW;
+  static constexpr int CAP = 4 * LPR;                    // list entries per window
+  static constexpr int GROUP_BYTES = 2 * STAGE + CAP * 8;
+  static constexpr int CTA_BYTES = 8 * (32 / LPR) * GROUP_BYTES;
+};
+
+template <typename T, int LPR, bool ALIGNED>
+__device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyItem& it, int cols, int gl,
+                                             unsigned gmask, uint8_t* stage, int2* list) {
+  using S = Skinny1Smem<T, LPR>;
+  constexpr int VEC = 16 / sizeof(T);
+  const int g = it.g;
+  const int n = it.n0 + gl * VEC;
+  const int p0 = a.row_partition[g], h = a.row_partition[g + 1] - p0;
+  const int b0 = a.blk_ptr[g];
+  const int hp = hp_of(h);
+  const int64_t dp = a.dp, ldb = a.ldb;
+  const T* tiles = static_cast<const T*>(a.tiles) + a.grp_tile_row[g] * dp;
+  const T* Bn = static_cast<const T*>(a.B) + n;
+
+  auto meta = [&](int bb, int& k0, int& w) {
+    k0 = 0;
+    w = 0;
+    if (gl < it.be - bb) {
+      const int bc = __ldg(a.blk_col + bb + gl);
+      k0 = __ldg(a.col_bounds + bc);
+      w = __ldg(a.col_bounds + bc + 1) - k0;
+    }
+  };
+  auto stage_issue = [&](int bb, uint8_t* buf, int w_lane) {
+    const int nbb = min(LPR, it.be - bb);
+#pragma unroll
+    for (int t = 0; t < S::PPB; ++t) {
+      const int q = t * LPR + gl;
+      const int j = q / S::PPB, pc = q - j * S::PPB;
+      const int wj = __shfl_sync(gmask, w_lane, j, LPR);
+      const bool pred = j < nbb && pc * VEC < wj;
+      cp_async16(buf + j * S::ROW + pc * 16, pred ? tiles + (int64_t)(bb - b0 + j) * hp * dp + pc * VEC : tiles, pred);
+    }
+    cp_async_commit();
+  };
+
+  float acc[1][VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[0][e] = 0.f;
+
+  int k0c, wc;
+  meta(it.bb, k0c, wc);
+  stage_issue(it.bb, stage, wc);
+  int buf = 0;
+  for (int bb = it.bb; bb < it.be; bb += LPR, buf ^= 1) {
+    const int nbb = min(LPR, it.be - bb);
+    const int bbn = bb + LPR;
+    int k0n = 0, wn = 0;
+    if (bbn < it.be) meta(bbn, k0n, wn);  // in flight while this batch is processed
+    uint8_t* cur = stage + buf * S::STAGE;
+    cp_async_wait_all();
+    __syncwarp(gmask);
+    // lane j: nonzero mask of staged row j
+    uint64_t msk = 0;
+    if (gl < nbb) {
+      const uint4* row = reinterpret_cast<const uint4*>(cur + gl * S::ROW);
+#pragma unroll
+      for (int pc = 0; pc < S::PPB; ++pc) {
+        const uint4 u = row[pc];
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if constexpr (sizeof(T) == 4) {
+            const int e = pc * 4 + i;
+            if (e < wc && (w4[i] & 0x7fffffffu)) msk |= 1ull << e;
+          } else {
+            const int e = pc * 8 + 2 * i;
+            if (e < wc && (w4[i] & 0x7fffu)) msk |= 1ull << e;
+            if (e + 1 < wc && (w4[i] & 0x7fff0000u)) msk |= 1ull << (e + 1);
+          }
+        }
+      }
+    }
+    const int cnt = __popcll(msk);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < LPR; d <<= 1) {
+      const int y = __shfl_up_sync(gmask, incl, d, LPR);
+      if (gl >= d) incl += y;
+    }
+    const int total = __shfl_sync(gmask, incl, LPR - 1, LPR);
+    const int excl = incl - cnt;
+    const T* myrow = reinterpret_cast<const T*>(cur + gl * S::ROW);
+    bool issued = false;
+    for (int base = 0; base < total; base += S::CAP) {
+      if (excl < base + S::CAP && incl > base) {
+        uint64_t m = msk;
+        int idx = excl;
+        while (m && idx < base + S::CAP) {
+          const int e = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          if (idx >= base) list[idx - base] = make_int2(k0c + e, __float_as_int(to_f(myrow[e])));
+          ++idx;
+        }
+      }
+      __syncwarp(gmask);
+      if (!issued && bbn < it.be) {  // next batch's rows land while this window's B rows are gathered
+        stage_issue(bbn, stage + (buf ^ 1) * S::STAGE, wn);
+        issued = true;
+      }
+      const int nh = min(S::CAP, total - base);
+      for (int i = 0; i < nh; i += 8) {
+        float av[8];
+        uint4 bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i + u < nh) {
+            const int2 en = list[i + u];
+            av[u] = __int_as_float(en.y);
+            bv[u] = load_b_raw<T, ALIGNED>(Bn + (int64_t)en.x * ldb, n, a.N);
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i + u < nh) fma_row<T>(acc[0], av[u], bv[u]);
+      }
+      __syncwarp(gmask);
+    }
+    if (!issued && bbn < it.be) stage_issue(bbn, stage + (buf ^ 1) * S::STAGE, wn);
+    k0c = k0n;
+    wc = wn;
+  }
+  skinny_finish<1, VEC, LPR, ALIGNED>(a, it, cols, h, p0, n, gl, gmask, acc);
+}
+
+template <typename T, int LPR, bool ALIGNED>
+__global__ void __launch_bounds__(256, 2) spmm_skinny1_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
+  using S = Skinny1Smem<T, LPR>;
+  constexpr int GPW = 32 / LPR;
+  extern __shared__ uint4 smem_sk[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
+  uint8_t* gbase = reinterpret_cast<uint8_t*>(smem_sk) + (warp * GPW + grp) * S::GROUP_BYTES;
+  int2* list = reinterpret_cast<int2*>(gbase + 2 * S::STAGE);
+  for (;;) {
+    const int64_t i = next_item<LPR>(sched, gl, gmask);
+    if (i >= a.n_items) break;
+    skinny1_item<T, LPR, ALIGNED>(a, load_item(a.items + i), cols, gl, gmask, gbase, list);
+  }
+  leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
+}
+
+// ---------------------------------------------------------------------------------------------
+// 2 <= h <= 8: per 32 (or 16) tile columns the lane group loads the h tile values of its column,
+// ballots the columns holding a nonzero in any of the h rows and gathers only those B rows
+// (four in flight), each B row feeding all h accumulators.
+template <typename T, int H, int LPR, bool ALIGNED>
+__device__ __forceinline__ void skinny_item(const SkinnyArgs& a, const SkinnyItem& it, int cols, int gl, int grp,
+                                            unsigned gmask) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int g = it.g;
+  const int n = it.n0 + gl * VEC;
+  const int p0 = a.row_partition[g], h = a.row_partition[g + 1] - p0;
+  const int b0 = a.blk_ptr[g];
+  const int hp = hp_of(h);
+  const int64_t dp = a.dp, ldb = a.ldb;
+  const T* tiles = static_cast<const T*>(a.tiles) + a.grp_tile_row[g] * dp;
+  const T* B = static_cast<const T*>(a.B) + n;
+
+  float acc[H][VEC];
+#pragma unroll
+  for (int r = 0; r < H; ++r)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[r][e] = 0.f;
+
+  for (int bb = it.bb; bb < it.be; bb += LPR) {
+    const int nbb = min(LPR, it.be - bb);
+    int my_k0 = 0, my_w = 0;
+    if (gl < nbb) {
+      const int bc = a.blk_col[bb + gl];
+      my_k0 = a.col_bounds[bc];
+      my_w = a.col_bounds[bc + 1] - my_k0;
+    }
+    for (int j = 0; j < nbb; ++j) {
+      const int k0 = __shfl_sync(gmask, my_k0, j, LPR);
+      const int w = __shfl_sync(gmask, my_w, j, LPR);
+      const T* t = tiles + (int64_t)(bb - b0 + j) * hp * dp;
+      for (int kc = 0; kc < w; kc += LPR) {
+        const int k = kc + gl;
+        float v[H];
+        bool nz = false;
+#pragma unroll
+        for (int r = 0; r < H; ++r) {
+          v[r] = (r < h && k < w) ? to_f(t[r * dp + k]) : 0.f;
+          nz |= v[r] != 0.f;
+        }
+        unsigned m = __ballot_sync(gmask, nz);
+        if (LPR < 32) m = (m >> (grp * LPR)) & ((1u << LPR) - 1u);
+        const T* brow = B + (int64_t)(k0 + kc) * ldb;
+        while (m) {
+          int kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            kk[u] = m ? __ffs(m) - 1 : -1;
+            m &= m - 1;
+          }
+          uint4 bv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (kk[u] >= 0) bv[u] = load_b_raw<T, ALIGNED>(brow + kk[u] * ldb, n, a.N);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (kk[u] < 0) break;
+#pragma unroll
+            for (int r = 0; r < H; ++r) fma_row<T>(acc[r], __shfl_sync(gmask, v[r], kk[u], LPR), bv[u]);
+          }
+        }
+      }
+    }
+  }
+  skinny_finish<H, VEC, LPR, ALIGNED>(a, it, cols, h, p0, n, gl, gmask, acc);
+}
+
+template <typename T, int H, int LPR, bool ALIGNED>
+__global__ void __launch_bounds__(256, H >= 8 ? 1 : 2) spmm_skinny_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
+  constexpr int GPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
+  for (;;) {
+    const int64_t i = next_item<LPR>(sched, gl, gmask);
+    if (i >= a.n_items) break;
+    skinny_item<T, H, LPR, ALIGNED>(a, load_item(a.items + i), cols, gl, grp, gmask);
+  }
+  leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
+}
+
+template <typename K>
+int persistent_grid(K kernel, int smem, int64_t n_items, int groups_per_cta, unsigned* grid) {
+  int dev = 0, sms = kNumSMs, per_sm = 1;
+  RB_CUDA_TRY(cudaGetDevice(&dev));
+  RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  RB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem));
+  const int64_t need = (n_items + groups_per_cta - 1) / groups_per_cta;
+  *grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * std::max(1, per_sm)));
+  return RB_OK;
+}
+
+template <typename T, int H, int LPR>
+int launch_t(const SkinnyArgs& a, int cols, unsigned long long* sched, cudaStream_t stream) {
+  const bool aligned = ((a.ldb * (int64_t)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0) &&
+                       (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
+  constexpr int per_cta = 8 * (32 / LPR);
+  unsigned grid = 0;
+  if constexpr (H == 1) {
+    using S = Skinny1Smem<T, LPR>;
+    if (a.dp > S::KC) {  // wide tiles: the generic kernel
+      auto k = aligned ? spmm_skinny_kernel<T, 1, LPR, true> : spmm_skinny_kernel<T, 1, LPR, false>;
+      int rc = persistent_grid(k, 0, a.n_items, per_cta, &grid);
+      if (rc) return rc;
+      k<<<grid, 256, 0, stream>>>(a, cols, sched);
+      RB_CUDA_TRY(cudaGetLastError());
+      return RB_OK;
+    }
+    auto k = aligned ? spmm_skinny1_kernel<T, LPR, true> : spmm_skinny1_kernel<T, LPR, false>;
+    RB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::CTA_BYTES));
+    int rc = persistent_grid(k, S::CTA_BYTES, a.n_items, per_cta, &grid);
+    if (rc) return rc;
+    k<<<grid, 256, S::CTA_BYTES, stream>>>(a, cols, sched);
+  } else {
+    auto k = aligned ? spmm_skinny_kernel<T, H, LPR, true> : spmm_skinny_kernel<T, H, LPR, false>;
+    int rc = persistent_grid(k, 0, a.n_items, per_cta, &grid);
+    if (rc) return rc;
+    k<<<grid, 256, 0, stream>>>(a, cols, sched);
+  }
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}
+
+template <typename T, int LPR>
+int launch_h(const SkinnyArgs& a, int cls, int cols, unsigned long long* sched, cudaStream_t stream) {
+  switch (cls) {
+    case 0: return launch_t<T, 1, LPR>(a, cols, sched, stream);
+    case 1: return launch_t<T, 2, LPR>(a, cols, sched, stream);
+    case 2: return launch_t<T, 4, LPR>(a, cols, sched, stream);
+    default: return launch_t<T, 8, LPR>(a, cols, sched, stream);
+  }
+}
+
+}  // namespace
+
+int skinny_cols(int32_t b_dtype, int64_t N) {
+  if (b_dtype == RB_F32) return 128;  // 32 lanes x 4
+  return N <= 128 ? 128 : 256;        // 16 or 32 lanes x 8
+}
+
+void skinny_items_for_row(int32_t g, int h, int32_t blk_begin, int nb, int64_t N, int cols,
+                          std::vector<SkinnyItem>& out, int64_t& n_slots, int64_t& ws_units) {
+  const int H = skinny_class_h(skinny_class(h));
+  const int nparts = nb > SKINNY_PART_BLOCKS ? (nb + SKINNY_PART_BLOCKS - 1) / SKINNY_PART_BLOCKS : 1;
+  for (int64_t n0 = 0; n0 < N; n0 += cols) {
+    if (nparts == 1) {
+      out.push_back(SkinnyItem{g, (int32_t)n0, blk_begin, blk_begin + nb, 0, 1, -1, 0});
+      continue;
+    }
+    const int32_t slot = (int32_t)n_slots++;
+    const int32_t wsoff = (int32_t)ws_units;
+    ws_units += (int64_t)nparts * H * (cols / 128);
+    for (int p = 0; p < nparts; ++p)
+      out.push_back(SkinnyItem{g, (int32_t)n0, blk_begin + (int32_t)((int64_t)nb * p / nparts),
+                               blk_begin + (int32_t)((int64_t)nb * (p + 1) / nparts), p, nparts, slot, wsoff});
+  }
+}
+
+int launch_skinny(const SkinnyArgs& a, int32_t b_dtype, int cls, unsigned long long* sched, cudaStream_t stream) {
+  if (a.n_items <= 0) return RB_OK;
+  const int cols = skinny_cols(b_dtype, a.N);
+  switch (b_dtype) {
+    case RB_F32: return launch_h<float, 32>(a, cls, cols, sched, stream);
+    case RB_BF16:
+      return a.N <= 128 ? launch_h<__nv_bfloat16, 16>(a, cls, cols, sched, stream)
+                        : launch_h<__nv_bfloat16, 32>(a, cls, cols, sched, stream);
+    case RB_F16:
+      return a.N <= 128 ? launch_h<__half, 16>(a, cls, cols, sched, stream)
+                        : launch_h<__half, 32>(a, cls, cols, sched, stream);
+    default: return fail(RB_EUNSUPPORTED, "skinny SpMM: unsupported dtype");
+  }
+}
+
+}  // namespace rb

@@ -292,3 +292,96 @@ def test_spmm_tall_split_k_tail(split, monkeypatch):
     assert torch.equal(C1, C2)
     Ad = A.to_dense()
     assert_close(C1.cpu().numpy().astype(np.float64), Ad @ B, np.abs(Ad) @ np.abs(B), 1e-4, f"split={split}")
+
+
+def _grouped_matrix(rng, heights, n_cols, delta, density):
+    """A matrix whose block rows are given (heights), scrambled rows, ragged last segment."""
+    from paper_2202_05868_b200.types import csr_from_coo
+
+    n_rows = int(sum(heights))
+    keys = np.unique(rng.choice(n_rows * n_cols, size=int(density * n_rows * n_cols), replace=False))
+    vals = rounded(rng.uniform(0.1, 1.0, len(keys)), torch.bfloat16) * rng.choice([-1.0, 1.0], len(keys))
+    A = csr_from_coo(n_rows, n_cols, keys // n_cols, keys % n_cols, vals)
+    perm = torch.from_numpy(rng.permutation(n_rows)).cuda()
+    rp = torch.tensor(np.concatenate([[0], np.cumsum(heights)]), device="cuda")
+    return A, perm, rp
+
+
+@pytest.mark.parametrize("precision,N,ld", [("fp32", 37, 37), ("fp32", 256, 256), ("bf16", 100, 104),
+                                            ("bf16", 300, 304), ("fp16", 64, 64)])
+def test_spmm_skinny_block_rows(precision, N, ld, monkeypatch):
+    """Block rows with h <= 8 run on the CUDA-core skinny kernel (every height class, lane groups of
+    16 and 32, unaligned fp32 B rows, ragged N, empty block rows).  C within tolerance of the
+    float64 product of the same rounded inputs; on the fp32 path bit-identical to the dense-tile
+    SIMT kernel (RB_SKINNY_H=0), since the skipped terms are exact zeros."""
+    from paper_2202_05868_b200 import _lib as L
+    from paper_2202_05868_b200.device import DeviceCsr, DeviceVbr
+
+    rng = np.random.default_rng(23)
+    heights = [1, 2, 3, 4, 5, 8, 1, 1, 7, 2] * 6 + [40, 200]
+    A, perm, rp = _grouped_matrix(rng, heights, 700, 48, 0.03)
+    q = rb.ColumnPartition.uniform(700, 48)
+    dt = L.TORCH_DTYPE[L.PRECISION[precision]]
+    Bh = rounded(rng.uniform(-1, 1, (700, N)), dt if dt != torch.float32 else torch.bfloat16)
+    Bd = torch.zeros((700, ld), dtype=dt, device="cuda")[:, :N]
+    Bd.copy_(torch.from_numpy(Bh))
+    Cs = {}
+    for sk in ["8", "0"]:
+        monkeypatch.setenv("RB_SKINNY_H", sk)
+        dv = DeviceVbr.build(DeviceCsr.from_host(A, "cuda"), q, perm, rp, dtypes=(precision,))
+        info = dv.plan_info(N, precision)
+        assert (info["n_items_skinny"] > 0) == (sk == "8")
+        Cs[sk] = dv.spmm(Bd, precision=precision)
+        torch.cuda.synchronize()
+        assert torch.equal(Cs[sk], dv.spmm(Bd, precision=precision))
+    Ad = dense_of({"n_rows": A.n_rows, "n_cols": A.n_cols, "row_ptr": A.row_ptr, "col_idx": A.col_idx,
+                   "values": A.values}, None if precision != "fp16" else torch.float16)
+    ref = Ad @ Bh
+    bound = np.abs(Ad) @ np.abs(Bh)
+    tol = 1e-5 if precision == "fp32" else 1e-4
+    assert_close(Cs["8"].cpu().numpy().astype(np.float64), ref, bound, tol, f"skinny {precision}")
+    if precision == "fp32":
+        assert torch.equal(Cs["8"], Cs["0"])
+    else:
+        assert_close(Cs["0"].cpu().numpy().astype(np.float64), ref, bound, tol, f"tensor {precision}")
+
+
+@pytest.mark.parametrize("precision,N", [("fp32", 256), ("bf16", 128), ("bf16", 520)])
+def test_spmm_skinny_split_rows(precision, N):
+    """Skinny block rows with more than 256 stored blocks (power-law hubs) are cut into parts whose
+    partials are summed in part order by the last-arriving part: C within tolerance and
+    bit-identical run to run (the arrival counters reset themselves between launches)."""
+    from paper_2202_05868_b200 import _lib as L
+    from paper_2202_05868_b200.device import DeviceCsr, DeviceVbr
+    from paper_2202_05868_b200.types import csr_from_coo
+
+    rng = np.random.default_rng(29)
+    n_cols, delta = 40000, 64
+    heights = [1, 1, 3, 1, 8, 2, 1]
+    per_row = [3000, 40, 900, 1200, 500, 2500, 5]
+    rows, cols, r0 = [], [], 0
+    for h, k in zip(heights, per_row):
+        for r in range(r0, r0 + h):
+            c = rng.choice(n_cols, size=k, replace=False)
+            rows.append(np.full(k, r))
+            cols.append(c)
+        r0 += h
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    vals = rounded(rng.uniform(0.1, 1.0, len(rows)), torch.bfloat16) * rng.choice([-1.0, 1.0], len(rows))
+    A = csr_from_coo(r0, n_cols, rows, cols, vals)
+    perm = torch.from_numpy(rng.permutation(r0)).cuda()
+    rp = torch.tensor(np.concatenate([[0], np.cumsum(heights)]), device="cuda")
+    q = rb.ColumnPartition.uniform(n_cols, delta)
+    dv = DeviceVbr.build(DeviceCsr.from_host(A, "cuda"), q, perm, rp, dtypes=(precision,))
+    _, bp, _ = dv.host_structure()
+    assert np.diff(bp).max() > 512  # several parts
+    dt = L.TORCH_DTYPE[L.PRECISION[precision]]
+    Bh = rounded(rng.uniform(-1, 1, (n_cols, N)), torch.bfloat16)
+    Bd = torch.from_numpy(Bh).cuda().to(dt)
+    C1 = dv.spmm(Bd, precision=precision)
+    C2 = dv.spmm(Bd, precision=precision)
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)
+    Ad = A.to_dense()
+    tol = 1e-5 if precision == "fp32" else 1e-4
+    assert_close(C1.cpu().numpy().astype(np.float64), Ad @ Bh, np.abs(Ad) @ np.abs(Bh), tol, "split rows")
