@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--e2e-steps", type=int, default=10)
     return p.parse_args()
 
 
@@ -299,16 +299,32 @@ def run_ours(args, world, rank):
     peaks = measured_peaks()
     achieved_tflops = useful / (ms_local * 1e-3) / 1e12 if world == 1 else useful / (ms * 1e-3) / 1e12
     exec_tflops = info["executed_flops"] / (ms_local * 1e-3) / 1e12
-    roof = {"bound": "tensor", "kernel": "spmm_tall2_kernel" if info["n_items_tall"] else "spmm_short2_kernel",
-            "achieved": round(achieved_tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": round(achieved_tflops / peaks["bf16_tflops"], 5), "traffic": profile_traffic(args.config),
-            "peak_source": peaks["source"] + " (burst bf16, kernel timed alone)",
-            "algorithmic": "2*nnz*N flops per launch",
-            "executed_tflops": round(exec_tflops, 3),
-            "executed_frac": round(exec_tflops / peaks["bf16_tflops"], 4),
-            "executed_flops_per_launch": info["executed_flops"]}
-    if prec == "fp32":
-        roof.update(bound="hbm", kernel="spmm_simt_f32_kernel")
+    tensor_dominant = prec != "fp32" and info["core_vbr_flops"] < 0.5 * info["vbr_flops"]
+    if tensor_dominant:
+        roof = {"bound": "tensor", "kernel": "spmm_tall2_kernel" if info["n_items_tall"] else "spmm_short2_kernel",
+                "achieved": round(achieved_tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": round(achieved_tflops / peaks["bf16_tflops"], 5), "traffic": profile_traffic(args.config),
+                "peak_source": peaks["source"] + " (burst bf16, kernel timed alone)",
+                "algorithmic": "2*nnz*N flops per launch",
+                "executed_tflops": round(exec_tflops, 3),
+                "executed_frac": round(exec_tflops / peaks["bf16_tflops"], 4),
+                "executed_flops_per_launch": info["executed_flops"]}
+    else:
+        # CUDA-core (skinny / fp32) kernels gather B rows: HBM roofline on the minimal traffic of the
+        # product — A read once (nnz x (value + 4 B column)), B read once, C written once (fp32).
+        esz = 4 if prec == "fp32" else 2
+        alg_bytes = dA.nnz * (esz + 4) + dA.n_cols * N * esz + dA.n_rows * N * 4
+        ms_ach = ms_local if world == 1 else ms
+        achieved_gbs = alg_bytes / (ms_ach * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "spmm_skinny1_kernel (+ skinny H=2..8)" if prec != "fp32"
+                else "spmm_skinny*_kernel<float> + spmm_simt_f32_kernel",
+                "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved_gbs / peaks["hbm_gbs"], 5), "traffic": profile_traffic(args.config),
+                "peak_source": peaks["source"] + " (HBM copy bandwidth)",
+                "algorithmic": "nnz*(elem+4) + n_cols*N*elem + n_rows*N*4 bytes per step (all launches)",
+                "algorithmic_bytes_per_step": alg_bytes,
+                "executed_tflops": round(exec_tflops, 3),
+                "useful_tflops": round(achieved_tflops, 4)}
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
@@ -330,44 +346,51 @@ def run_ours(args, world, rank):
 
 
 def run_e2e(args, dv, dA, B, prec, rank, world):
-    """Steps through the reference-facing host path: H2D of the step's B (float64, pinned, as the
-    reference's DenseMatrix), conversion + SpMM on the device, D2H of C (float64, pinned)."""
-    from paper_2202_05868_b200 import _lib as L
+    """Steps through the public host-buffer API (multiply.SpmmPipeline, what spmm_vbr_many runs):
+    every step copies its float64 B from pinned host memory to the device, converts it, runs the
+    SpMM, widens C to float64 and copies it back to pinned host memory (the reference's
+    DenseMatrix contract, matrix.py:107-111).  Steps overlap on three streams (B of step k+1 in,
+    SpMM of step k, C of step k-1 out); the timed region spans the first copy in to the last copy
+    out, so every step's transfers are inside it."""
+    from paper_2202_05868_b200.multiply import SpmmPipeline, pinned_dense
 
     N = B.shape[1]
-    K = B.shape[0]
-    B_host = B.double().cpu().pin_memory()
-    C_host = torch.empty((dA.n_rows, N), dtype=torch.float64).pin_memory()
-    dev = B.device
-    B_dev64 = torch.empty((K, N), dtype=torch.float64, device=dev)
-    ld = (N + 7) // 8 * 8
-    B_k = torch.empty((K, ld), dtype=L.TORCH_DTYPE[L.PRECISION[prec]], device=dev)
-    C32 = torch.empty((dA.n_rows, N), dtype=torch.float32, device=dev)
-    C64 = torch.empty((dA.n_rows, N), dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream()
-    lib = L.lib()
-
-    def step():
-        B_dev64.copy_(B_host, non_blocking=True)
-        L.check(lib.rb_convert_f64(L.ptr(B_dev64), K, N, N, L.ptr(B_k), L.PRECISION[prec], ld, L.stream_handle()))
-        dv.spmm(B_k[:, :N], out=C32, precision=prec, shard=rank, n_shards=world)
-        L.check(lib.rb_widen_f32(L.ptr(C32), dA.n_rows, N, N, L.ptr(C64), N, L.stream_handle()))
-        C_host.copy_(C64, non_blocking=True)
-
-    for _ in range(2):
-        step()
+    B_host = [B.double().cpu().pin_memory() for _ in range(2)]
+    C_host = [pinned_dense(dA.n_rows, N) for _ in range(2)]
+    pipe = SpmmPipeline(dv, N, prec)
+    if world > 1:  # each rank runs its own shard of every product
+        pipe.dv = _ShardView(dv, rank, world)
+    for k in range(2):
+        pipe.step(k, B_host[k % 2], C_host[k % 2])
+    pipe.synchronize()
     torch.cuda.synchronize()
     barrier(world)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record(stream)
-    for _ in range(args.e2e_steps):
-        step()
-    e.record(stream)
+    s.record(pipe.s_in)
+    for k in range(args.e2e_steps):
+        pipe.step(k, B_host[k % 2], C_host[k % 2])
+    e.record(pipe.s_out)
     torch.cuda.synchronize()
     ms = allreduce_max(s.elapsed_time(e) / args.e2e_steps, world)
     return {"value": round(2.0 * dA.nnz * N / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(ms, 4),
-            "h2d_bytes_per_step": int(B_host.numel() * 8), "d2h_bytes_per_step": int(C_host.numel() * 8),
-            "path": "pinned float64 B -> H2D -> rb_convert_f64 -> rb_spmm_execute -> rb_widen_f32 -> D2H float64 C"}
+            "h2d_bytes_per_step": int(B_host[0].numel() * 8), "d2h_bytes_per_step": int(C_host[0].numel() * 8),
+            "steps": args.e2e_steps,
+            "path": "SpmmPipeline (spmm_vbr_many): pinned float64 B -> H2D -> rb_convert_f64 -> rb_spmm_execute "
+                    "-> rb_widen_f32 -> D2H float64 C, steps overlapped on 3 streams"}
+
+
+class _ShardView:
+    """DeviceVbr facade that runs only this rank's shard of the plan."""
+
+    def __init__(self, dv, rank, world):
+        self._dv, self._rank, self._world = dv, rank, world
+        self.n_rows, self.n_cols = dv.n_rows, dv.n_cols
+
+    def plan(self, N, precision="bf16", stream=None):
+        return self._dv.plan(N, precision, self._rank, self._world, stream)
+
+    def spmm(self, B, out=None, precision=None, stream=None):
+        return self._dv.spmm(B, out=out, precision=precision, shard=self._rank, n_shards=self._world, stream=stream)
 
 
 def run_reference(args, world, rank):

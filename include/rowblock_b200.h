@@ -147,6 +147,7 @@ typedef struct rb_spmm_info {
   int64_t row_begin_perm;    /* first permuted row covered by this shard (or -1 if empty) */
   int64_t n_items_skinny;    /* (block row, C-column slab) CUDA-core items for block rows with h <= 8 */
   int64_t n_launches;        /* kernel launches per rb_spmm_execute */
+  double core_vbr_flops;     /* part of vbr_flops run on the CUDA cores (skinny / fp32 kernels) */
 } rb_spmm_info;
 
 int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t b_dtype, int32_t shard,

@@ -729,7 +729,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
     if (rc) return rc;
   }
   std::vector<int4> tall, shrt, simt;
-  double exec_flops = 0, vbr_flops = 0;
+  double exec_flops = 0, vbr_flops = 0, core_vbr_flops = 0;
   const int dpc = tc ? vbr->dp / KCH : 1;
   // short items: item order n-chunk-major keeps one 256-column B slab hot in L2 while A tiles stream
   // (RB_SHORT_ORDER=g switches to block-row-major)
@@ -756,12 +756,14 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       skinny_items_for_row((int32_t)g, h, bp[g], nb, N, sk_cols, skinny[skinny_class(h)], sk_slots, sk_units);
       exec_flops += 2.0 * nb * h * (double)vbr->dp * N;
       vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
+      core_vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
     } else if (!tc) {
       for (int r0 = 0; r0 < h; r0 += SIMT_ROWS) {
         if (rp[g] + r0 < row_lo || rp[g] + r0 >= row_hi) continue;
         for (int64_t n0 = 0; n0 < N; n0 += SIMT_COLS) simt.push_back(make_int4((int)g, r0, (int)n0, nb));
         exec_flops += 2.0 * nb * std::min(SIMT_ROWS, h - r0) * (double)vbr->dp * N;
         vbr_flops += 2.0 * nb * std::min(SIMT_ROWS, h - r0) * (double)vbr->dp * N;
+        core_vbr_flops += 2.0 * nb * std::min(SIMT_ROWS, h - r0) * (double)vbr->dp * N;
       }
     } else if (is_short_row(h)) {
       short_rows.push_back((int32_t)g);
@@ -874,6 +876,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   p->info.n_items_short = p->n_short;
   p->info.n_items_simt = p->n_simt;
   p->info.n_items_skinny = p->skinny_off[SKINNY_CLASSES];
+  p->info.core_vbr_flops = core_vbr_flops;
   p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0);
   for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   p->info.executed_flops = exec_flops;

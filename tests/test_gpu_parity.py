@@ -385,3 +385,18 @@ def test_spmm_skinny_split_rows(precision, N):
     Ad = A.to_dense()
     tol = 1e-5 if precision == "fp32" else 1e-4
     assert_close(C1.cpu().numpy().astype(np.float64), Ad @ Bh, np.abs(Ad) @ np.abs(Bh), tol, "split rows")
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_spmm_vbr_many_pipeline_matches_single(precision):
+    """The pipelined multi-RHS API (3 streams, double-buffered) returns, for every B_k, exactly
+    what spmm_vbr returns for that B alone (same plan, same kernels), in order."""
+    case = load_golden("cfg5_s32")
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    rng = np.random.default_rng(31)
+    Bs = [rb.DenseMatrix.from_array(rng.random((A.n_cols, 96))) for _ in range(5)]
+    many = rb.spmm_vbr_many(V, Bs, precision=precision)
+    assert len(many) == 5
+    for B, C in zip(Bs, many):
+        assert np.array_equal(C.data, rb.spmm_vbr(V, B, precision=precision).data)
