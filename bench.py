@@ -295,6 +295,7 @@ def run_ours(args, world, rank):
 
     # ---- end to end through the reference-facing path: pinned float64 B -> device -> kernel -> float64 C
     e2e = run_e2e(args, dv, dA, B, prec, rank, world)
+    csr = run_csr_comparator(args, dA, B, prec, flush) if world == 1 else None
 
     peaks = measured_peaks()
     achieved_tflops = useful / (ms_local * 1e-3) / 1e12 if world == 1 else useful / (ms * 1e-3) / 1e12
@@ -316,7 +317,7 @@ def run_ours(args, world, rank):
         alg_bytes = dA.nnz * (esz + 4) + dA.n_cols * N * esz + dA.n_rows * N * 4
         ms_ach = ms_local if world == 1 else ms
         achieved_gbs = alg_bytes / (ms_ach * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "spmm_skinny1_kernel (+ skinny H=2..8)" if prec != "fp32"
+        roof = {"bound": "hbm", "kernel": "spmm_skinny_staged_kernel (h<=4 classes)" if prec != "fp32"
                 else "spmm_skinny*_kernel<float> + spmm_simt_f32_kernel",
                 "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved_gbs / peaks["hbm_gbs"], 5), "traffic": profile_traffic(args.config),
@@ -334,6 +335,7 @@ def run_ours(args, world, rank):
                    "parallelism": f"block-row shards x{world}" if world > 1 else "single GPU",
                    "l2": "flushed between steps (256 MiB memset outside the timed events)"},
         "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+        "csr_comparator": csr,
         "clocks": sampler.summary(),
         "stages": dict(stages, rho_prime=round(dA.nnz / max(dv.stored_area(), 1), 5),
                        padding_executed_over_useful=round(info["executed_flops"] * world / useful, 3),
@@ -343,6 +345,25 @@ def run_ours(args, world, rank):
         out["cpu_baseline"] = cpu_baseline(dA, bounds, dv, B, args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def run_csr_comparator(args, dA, B, prec, flush):
+    """The paper's sparse baseline on the same device and inputs: spmm_csr (multiply.py:51-69) as
+    the CSR gather kernel (csrc/csr.cu), same B, same L2 flush; not part of the headline value."""
+    C = torch.empty((dA.n_rows, B.shape[1]), dtype=torch.float32, device=B.device)
+    for _ in range(2):
+        dA.spmm(B, out=C, precision=prec)
+    steps = max(3, min(args.steps, 10))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for s, e in ev:
+        flush.zero_()
+        s.record()
+        dA.spmm(B, out=C, precision=prec)
+        e.record()
+    torch.cuda.synchronize()
+    ms = sum(s.elapsed_time(e) for s, e in ev) / steps
+    return {"kernel": "spmm_csr_kernel", "ms_per_step": round(ms, 5),
+            "value": round(2.0 * dA.nnz * B.shape[1] / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s"}
 
 
 def run_e2e(args, dv, dA, B, prec, rank, world):

@@ -163,6 +163,38 @@ int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* blk_ptr, in
                         int32_t b_dtype, int32_t dp, int32_t shard, int32_t n_shards, int64_t* row_begin,
                         int64_t* row_end);
 
+/* ------------------------------------------------------------------ spmm_csr
+ * GPU comparator for spmm_csr(A, B, threads) (multiply.py:51-69): C = A·B straight from the
+ * reference's CSR arrays (row_ptr/col_idx int64, values float64, device), C float32 [n_rows x N]
+ * in row order (rows without nonzeros are exact zeros).  B as for rb_spmm_execute (RB_BF16/RB_F16/
+ * RB_F32).  The plan (work list from a host copy of row_ptr) is reusable across B.            */
+typedef struct rb_csr_plan rb_csr_plan;
+int rb_csr_plan_create(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, int64_t n_dense_cols,
+                       int32_t b_dtype, rb_csr_plan** plan, void* stream);
+int rb_csr_execute(const rb_csr_plan* plan, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                   const void* B, int64_t ldb, float* C, int64_t ldc, void* stream);
+int rb_csr_plan_destroy(rb_csr_plan* plan);
+
+/* ------------------------------------------------------------------ blocking_stats / verify_density_bound
+ * Replace blocking_stats (metrics.py:59-95) and verify_density_bound (metrics.py:178-216) for a
+ * grouping in device memory (row_perm[n_rows] / group_ptr[H+1] as returned by rb_block_1sa,
+ * pattern_ptr[H+1] / pattern_idx = RowGroup.pattern).  Per group g (device outputs, [H]):
+ *   stored_cols[g]  = sum of the pattern's segment widths
+ *   element_nnz[g]  = sum of the member rows' nnz
+ *   quotient_nnz[g] = sum of the member rows' distinct segment counts
+ *   ok[g]           = bit0 element_ok, bit1 quotient_ok, the reference's exact rational tests
+ *                     k_elem/(h*stored_cols) >= tau/(2*max_width), k_quot/(h*lambda) >= tau/2
+ *                     (empty patterns pass).
+ * HOST totals: stored area, stored blocks, sum over blocks of the block height, violations.
+ * Workspace: rb_group_stats_workspace_size.                                              */
+int rb_group_stats_workspace_size(int64_t n_seg, size_t* bytes);
+int rb_group_stats(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                   const int64_t* boundaries, int64_t n_seg, const int64_t* row_perm, const int64_t* group_ptr,
+                   const int64_t* pattern_ptr, const int64_t* pattern_idx, int64_t n_groups, double tau,
+                   void* workspace, size_t workspace_bytes, int64_t* stored_cols, int64_t* element_nnz,
+                   int64_t* quotient_nnz, uint8_t* ok, int64_t* stored_area, int64_t* n_blocks,
+                   int64_t* height_sum, int64_t* n_violations, void* stream);
+
 /* ------------------------------------------------------------------ helpers
  * Element conversion used by the drop-in path (DenseMatrix is float64, matrix.py:107-111):
  * dst[r, c] (row stride ldd, dtype dst_dtype) = src[r, c] (float64, row stride lds).   */

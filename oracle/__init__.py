@@ -228,3 +228,42 @@ def spmm_csr_np(row_ptr, col_idx, values, B: np.ndarray) -> np.ndarray:
         if e > s:
             C[i] = values[s:e] @ B[col_idx[s:e]]
     return C
+
+
+def group_stats_np(row_ptr, col_idx, boundaries, row_perm, group_ptr, pattern_ptr, pattern_idx, tau):
+    """Restatement of blocking_stats (metrics.py:59-95) and verify_density_bound (metrics.py:178-216)
+    on grouping arrays: per group stored columns, element nnz, quotient nnz (popcount of the
+    quotient bits, blocking.py:118-136) and the exact Fraction verdicts; plus the totals."""
+    from fractions import Fraction
+
+    rp = np.asarray(row_ptr, np.int64)
+    b = np.asarray(boundaries, np.int64)
+    widths = np.diff(b)
+    max_w = int(widths.max()) if len(widths) else 1
+    _, qsizes = quotient(rp, col_idx, b)
+    row_nnz = np.diff(rp)
+    f_tau = Fraction(float(tau))
+    eb, qb = f_tau / (2 * max_w), f_tau / 2
+    gp, pp = np.asarray(group_ptr, np.int64), np.asarray(pattern_ptr, np.int64)
+    perm, pats = np.asarray(row_perm, np.int64), np.asarray(pattern_idx, np.int64)
+    H = len(gp) - 1
+    out = {k: np.zeros(H, np.int64) for k in ("stored_cols", "element_nnz", "quotient_nnz")}
+    out["element_ok"] = np.ones(H, bool)
+    out["quotient_ok"] = np.ones(H, bool)
+    area = blocks = hsum = 0
+    for g in range(H):
+        rows = perm[gp[g]:gp[g + 1]]
+        pat = pats[pp[g]:pp[g + 1]]
+        h, lam = len(rows), len(pat)
+        sc = int(widths[pat].sum()) if lam else 0
+        ke, kq = int(row_nnz[rows].sum()), int(np.asarray(qsizes)[rows].sum())
+        out["stored_cols"][g], out["element_nnz"][g], out["quotient_nnz"][g] = sc, ke, kq
+        area += h * sc
+        blocks += lam
+        hsum += h * lam
+        if lam:
+            out["element_ok"][g] = Fraction(ke, h * sc) >= eb
+            out["quotient_ok"][g] = Fraction(kq, h * lam) >= qb
+    out.update(stored_area=area, n_blocks=blocks, height_sum=hsum, nnz=int(rp[-1]), n_groups=H,
+               element_bound=float(eb), quotient_bound=float(qb))
+    return out

@@ -15,14 +15,17 @@ there is no CPU fallback.  The torch-native, HBM-resident API is in ``device``.
 from .blocking import block_1sa
 from .config import default_precision, set_default_precision
 from .device import DeviceCsr, DeviceGrouping, DeviceVbr, block_1sa_device
-from .multiply import SpmmPipeline, pinned_dense, spmm_vbr, spmm_vbr_device, spmm_vbr_many
+from .metrics import (BlockingCurve, BlockingStats, DensityReport, GroupDensity, blocking_curve, blocking_stats,
+                      curve_select, verify_density_bound)
+from .multiply import SpmmPipeline, pinned_dense, spmm_csr, spmm_vbr, spmm_vbr_device, spmm_vbr_many
 from .types import (ColumnPartition, CsrMatrix, DenseMatrix, MergePolicy, RowGroup, RowGrouping, VbrBlock,
                     VbrMatrix, csr_from_triplets)
 from .vbr import vbr_from_grouping
 
 __all__ = [
     "block_1sa", "vbr_from_grouping", "spmm_vbr", "spmm_vbr_many", "spmm_vbr_device", "block_1sa_device",
-    "SpmmPipeline", "pinned_dense",
+    "SpmmPipeline", "pinned_dense", "spmm_csr", "blocking_stats", "blocking_curve", "curve_select",
+    "verify_density_bound", "BlockingStats", "BlockingCurve", "GroupDensity", "DensityReport",
     "DeviceCsr", "DeviceGrouping", "DeviceVbr", "ColumnPartition", "CsrMatrix", "DenseMatrix", "MergePolicy",
     "RowGroup", "RowGrouping", "VbrBlock", "VbrMatrix", "csr_from_triplets", "default_precision",
     "set_default_precision",

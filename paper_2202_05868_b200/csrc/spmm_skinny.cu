@@ -57,6 +57,22 @@ __device__ __forceinline__ uint4 load_b_raw(const T* p, int n, int N) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// float64 -> operand dtype (round to nearest even, as the VBR tile emission does) -> float
+template <typename T>
+__device__ __forceinline__ float round_to(double v);
+template <>
+__device__ __forceinline__ float round_to<__nv_bfloat16>(double v) {
+  return __bfloat162float(__double2bfloat16(v));
+}
+template <>
+__device__ __forceinline__ float round_to<__half>(double v) {
+  return __half2float(__double2half(v));
+}
+template <>
+__device__ __forceinline__ float round_to<float>(double v) {
+  return (float)v;
+}
+
 template <typename T>
 __device__ __forceinline__ float elem(const uint4& u, int e) {
   if constexpr (sizeof(T) == 4) {
@@ -142,7 +158,10 @@ __device__ __forceinline__ void skinny_finish(const SkinnyArgs& a, const SkinnyI
   if (n >= a.N) return;
 #pragma unroll
   for (int r = 0; r < H; ++r)
-    if (r < h) store_c<VEC, ALIGNED>(a.C + (int64_t)a.row_perm[p0 + r] * a.ldc + n, n, a.N, acc[r]);
+    if (r < h) {
+      const int64_t crow = a.row_perm ? (int64_t)a.row_perm[p0 + r] : (int64_t)p0 + r;  // CSR: identity
+      store_c<VEC, ALIGNED>(a.C + crow * a.ldc + n, n, a.N, acc[r]);
+    }
 }
 
 __device__ __forceinline__ SkinnyItem load_item(const SkinnyItem* p) {
@@ -170,13 +189,7 @@ __device__ __forceinline__ void leave(unsigned long long* sched, int gl, unsigne
 }
 
 // ---------------------------------------------------------------------------------------------
-// h == 1 (the common case on sparse inputs), tiles at most 64 columns wide.  Per batch of LPR
-// blocks the lane group
-//   * stages the blocks' tile rows in shared memory with cp.async (double buffered: the next
-//     batch's rows and block columns are in flight while this batch's B rows are gathered),
-//   * lane j turns staged row j into a 64-bit nonzero mask (16-byte shared loads, padded rows),
-//   * a group prefix sum orders the nonzeros (block ascending, k ascending) into a list,
-//   * the list is streamed with eight B-row gathers in flight per lane.
+// Staged kernel (tiles at most 64 columns wide, every height class), see staged_item below.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0) : "memory");
@@ -185,21 +198,33 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <typename T, int LPR>
-struct Skinny1Smem {
+struct SkinnySmem {
   static constexpr int KC = 64;                          // tile columns staged per block (dp <= 64)
   static constexpr int PPB = KC * (int)sizeof(T) / 16;   // 16-byte pieces per staged row
   static constexpr int ROW = KC * (int)sizeof(T) + 16;   // padded row stride: conflict-free row reads
-  static constexpr int STAGE = LPR * ROW;
+  static constexpr int STAGE = LPR * ROW;                // NB blocks x H rows = LPR staged rows
   static constexpr int CAP = 4 * LPR;                    // list entries per window
   static constexpr int GROUP_BYTES = 2 * STAGE + CAP * 8;
   static constexpr int CTA_BYTES = 8 * (32 / LPR) * GROUP_BYTES;
 };
 
-template <typename T, int LPR, bool ALIGNED>
-__device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyItem& it, int cols, int gl,
-                                             unsigned gmask, uint8_t* stage, int2* list) {
-  using S = Skinny1Smem<T, LPR>;
+// Block rows of height h <= H (H = 1, 2, 4, 8), tiles at most 64 columns wide.  Per batch of
+// NB = LPR / H blocks the lane group
+//   * stages the blocks' h tile rows in shared memory with cp.async (double buffered: the next
+//     batch's rows and block columns are in flight while this batch's B rows are gathered),
+//   * lane j turns block j's staged rows into the 64-bit mask of columns holding a nonzero in any
+//     row (16-byte shared loads, padded rows),
+//   * a group prefix sum orders those columns (block ascending, k ascending) into a list,
+//   * the list is streamed with DEPTH B-row gathers in flight per lane; each gathered B row feeds
+//     all h accumulators, the tile values coming from shared memory (broadcast reads).
+template <typename T, int H, int LPR, bool ALIGNED>
+__device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyItem& it, int cols, int gl,
+                                            unsigned gmask, uint8_t* stage, int2* list) {
+  using S = SkinnySmem<T, LPR>;
   constexpr int VEC = 16 / sizeof(T);
+  constexpr int NB = LPR / H;                 // blocks per batch
+  constexpr int DEPTH = H >= 4 ? 4 : 8;       // B gathers in flight per lane
+  constexpr int ROWE = S::ROW / (int)sizeof(T);
   const int g = it.g;
   const int n = it.n0 + gl * VEC;
   const int p0 = a.row_partition[g], h = a.row_partition[g + 1] - p0;
@@ -212,58 +237,67 @@ __device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyIt
   auto meta = [&](int bb, int& k0, int& w) {
     k0 = 0;
     w = 0;
-    if (gl < it.be - bb) {
+    if (gl < NB && gl < it.be - bb) {
       const int bc = __ldg(a.blk_col + bb + gl);
       k0 = __ldg(a.col_bounds + bc);
       w = __ldg(a.col_bounds + bc + 1) - k0;
     }
   };
   auto stage_issue = [&](int bb, uint8_t* buf, int w_lane) {
-    const int nbb = min(LPR, it.be - bb);
+    const int nbb = min(NB, it.be - bb);
 #pragma unroll
     for (int t = 0; t < S::PPB; ++t) {
       const int q = t * LPR + gl;
-      const int j = q / S::PPB, pc = q - j * S::PPB;
+      const int row = q / S::PPB, pc = q - row * S::PPB;  // staged row = j * H + r
+      const int j = row / H, r = row - j * H;
       const int wj = __shfl_sync(gmask, w_lane, j, LPR);
-      const bool pred = j < nbb && pc * VEC < wj;
-      cp_async16(buf + j * S::ROW + pc * 16, pred ? tiles + (int64_t)(bb - b0 + j) * hp * dp + pc * VEC : tiles, pred);
+      const bool pred = j < nbb && r < h && pc * VEC < wj;
+      cp_async16(buf + row * S::ROW + pc * 16,
+                 pred ? tiles + ((int64_t)(bb - b0 + j) * hp + r) * dp + pc * VEC : tiles, pred);
     }
     cp_async_commit();
   };
 
-  float acc[1][VEC];
+  float acc[H][VEC];
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) acc[0][e] = 0.f;
+  for (int r = 0; r < H; ++r)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[r][e] = 0.f;
 
   int k0c, wc;
   meta(it.bb, k0c, wc);
   stage_issue(it.bb, stage, wc);
   int buf = 0;
-  for (int bb = it.bb; bb < it.be; bb += LPR, buf ^= 1) {
-    const int nbb = min(LPR, it.be - bb);
-    const int bbn = bb + LPR;
+  for (int bb = it.bb; bb < it.be; bb += NB, buf ^= 1) {
+    const int nbb = min(NB, it.be - bb);
+    const int bbn = bb + NB;
     int k0n = 0, wn = 0;
     if (bbn < it.be) meta(bbn, k0n, wn);  // in flight while this batch is processed
     uint8_t* cur = stage + buf * S::STAGE;
+    const T* curT = reinterpret_cast<const T*>(cur);
     cp_async_wait_all();
     __syncwarp(gmask);
-    // lane j: nonzero mask of staged row j
+    // lane j: columns of block j holding a nonzero in any of its h staged rows
     uint64_t msk = 0;
     if (gl < nbb) {
-      const uint4* row = reinterpret_cast<const uint4*>(cur + gl * S::ROW);
 #pragma unroll
-      for (int pc = 0; pc < S::PPB; ++pc) {
-        const uint4 u = row[pc];
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+      for (int r = 0; r < H; ++r) {
+        if (r >= h) break;
+        const uint4* row = reinterpret_cast<const uint4*>(cur + (gl * H + r) * S::ROW);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if constexpr (sizeof(T) == 4) {
-            const int e = pc * 4 + i;
-            if (e < wc && (w4[i] & 0x7fffffffu)) msk |= 1ull << e;
-          } else {
-            const int e = pc * 8 + 2 * i;
-            if (e < wc && (w4[i] & 0x7fffu)) msk |= 1ull << e;
-            if (e + 1 < wc && (w4[i] & 0x7fff0000u)) msk |= 1ull << (e + 1);
+        for (int pc = 0; pc < S::PPB; ++pc) {
+          const uint4 u = row[pc];
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if constexpr (sizeof(T) == 4) {
+              const int e = pc * 4 + i;
+              if (e < wc && (w4[i] & 0x7fffffffu)) msk |= 1ull << e;
+            } else {
+              const int e = pc * 8 + 2 * i;
+              if (e < wc && (w4[i] & 0x7fffu)) msk |= 1ull << e;
+              if (e + 1 < wc && (w4[i] & 0x7fff0000u)) msk |= 1ull << (e + 1);
+            }
           }
         }
       }
@@ -277,7 +311,6 @@ __device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyIt
     }
     const int total = __shfl_sync(gmask, incl, LPR - 1, LPR);
     const int excl = incl - cnt;
-    const T* myrow = reinterpret_cast<const T*>(cur + gl * S::ROW);
     bool issued = false;
     for (int base = 0; base < total; base += S::CAP) {
       if (excl < base + S::CAP && incl > base) {
@@ -286,7 +319,10 @@ __device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyIt
         while (m && idx < base + S::CAP) {
           const int e = __ffsll((long long)m) - 1;
           m &= m - 1;
-          if (idx >= base) list[idx - base] = make_int2(k0c + e, __float_as_int(to_f(myrow[e])));
+          if (idx >= base) {  // (B row, value) for h == 1, else (B row, staged offset of column e)
+            const int y = H == 1 ? __float_as_int(to_f(curT[gl * ROWE + e])) : gl * H * ROWE + e;
+            list[idx - base] = make_int2(k0c + e, y);
+          }
           ++idx;
         }
       }
@@ -296,19 +332,27 @@ __device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyIt
         issued = true;
       }
       const int nh = min(S::CAP, total - base);
-      for (int i = 0; i < nh; i += 8) {
-        float av[8];
-        uint4 bv[8];
+      for (int i = 0; i < nh; i += DEPTH) {
+        int off[DEPTH];
+        uint4 bv[DEPTH];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < DEPTH; ++u)
           if (i + u < nh) {
             const int2 en = list[i + u];
-            av[u] = __int_as_float(en.y);
+            off[u] = en.y;
             bv[u] = load_b_raw<T, ALIGNED>(Bn + (int64_t)en.x * ldb, n, a.N);
           }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (i + u < nh) fma_row<T>(acc[0], av[u], bv[u]);
+        for (int u = 0; u < DEPTH; ++u)
+          if (i + u < nh) {
+            if constexpr (H == 1) {
+              fma_row<T>(acc[0], __int_as_float(off[u]), bv[u]);
+            } else {
+#pragma unroll
+              for (int r = 0; r < H; ++r)
+                if (r < h) fma_row<T>(acc[r], to_f(curT[off[u] + r * ROWE]), bv[u]);
+            }
+          }
       }
       __syncwarp(gmask);
     }
@@ -316,12 +360,12 @@ __device__ __forceinline__ void skinny1_item(const SkinnyArgs& a, const SkinnyIt
     k0c = k0n;
     wc = wn;
   }
-  skinny_finish<1, VEC, LPR, ALIGNED>(a, it, cols, h, p0, n, gl, gmask, acc);
+  skinny_finish<H, VEC, LPR, ALIGNED>(a, it, cols, h, p0, n, gl, gmask, acc);
 }
 
-template <typename T, int LPR, bool ALIGNED>
-__global__ void __launch_bounds__(256, 2) spmm_skinny1_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
-  using S = Skinny1Smem<T, LPR>;
+template <typename T, int H, int LPR, bool ALIGNED>
+__global__ void __launch_bounds__(256, H == 1 ? 2 : 1) spmm_skinny_staged_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
+  using S = SkinnySmem<T, LPR>;
   constexpr int GPW = 32 / LPR;
   extern __shared__ uint4 smem_sk[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
@@ -331,13 +375,13 @@ __global__ void __launch_bounds__(256, 2) spmm_skinny1_kernel(SkinnyArgs a, int 
   for (;;) {
     const int64_t i = next_item<LPR>(sched, gl, gmask);
     if (i >= a.n_items) break;
-    skinny1_item<T, LPR, ALIGNED>(a, load_item(a.items + i), cols, gl, gmask, gbase, list);
+    staged_item<T, H, LPR, ALIGNED>(a, load_item(a.items + i), cols, gl, gmask, gbase, list);
   }
   leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
 }
 
 // ---------------------------------------------------------------------------------------------
-// 2 <= h <= 8: per 32 (or 16) tile columns the lane group loads the h tile values of its column,
+// Wide tiles (dp > 64): per 32 (or 16) tile columns the lane group loads the h tile values of its column,
 // ballots the columns holding a nonzero in any of the h rows and gathers only those B rows
 // (four in flight), each B row feeding all h accumulators.
 template <typename T, int H, int LPR, bool ALIGNED>
@@ -420,6 +464,60 @@ __global__ void __launch_bounds__(256, H >= 8 ? 1 : 2) spmm_skinny_kernel(Skinny
   leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
 }
 
+// ---------------------------------------------------------------------------------------------
+// CSR comparator (spmm_csr, multiply.py:51-69): the same gather engine straight on a CSR row —
+// the sparse baseline the paper measures VBR against.  Item = (row, C-column slab, nonzero range);
+// per LPR nonzeros the group loads (column, value) coalesced, then gathers B rows 8 in flight.
+template <typename T, int LPR, bool ALIGNED>
+__device__ __forceinline__ void csr_item(const SkinnyArgs& a, const CsrArgs& c, const SkinnyItem& it, int cols, int gl,
+                                         unsigned gmask) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int n = it.n0 + gl * VEC;
+  const T* Bn = static_cast<const T*>(a.B) + n;
+  const int64_t ldb = a.ldb;
+  float acc[1][VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[0][e] = 0.f;
+  const int64_t base = c.row_ptr[it.g];
+  for (int64_t j0 = base + it.bb; j0 < base + it.be; j0 += LPR) {
+    const int cnt = (int)(base + it.be - j0 < LPR ? base + it.be - j0 : LPR);
+    int col = 0;
+    float val = 0.f;
+    if (gl < cnt) {
+      col = (int)__ldg(c.col_idx + j0 + gl);
+      val = round_to<T>(__ldg(c.values + j0 + gl));  // A rounded to the operand dtype, as in VBR tiles
+    }
+    for (int i = 0; i < cnt; i += 8) {
+      float av[8];
+      uint4 bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = __shfl_sync(gmask, col, (i + u) & (LPR - 1), LPR);
+        av[u] = __shfl_sync(gmask, val, (i + u) & (LPR - 1), LPR);
+        if (i + u < cnt) bv[u] = load_b_raw<T, ALIGNED>(Bn + (int64_t)k * ldb, n, a.N);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i + u < cnt) fma_row<T>(acc[0], av[u], bv[u]);
+    }
+  }
+  skinny_finish<1, VEC, LPR, ALIGNED>(a, it, cols, 1, it.g, n, gl, gmask, acc);
+}
+
+template <typename T, int LPR, bool ALIGNED>
+__global__ void __launch_bounds__(256, 2) spmm_csr_kernel(SkinnyArgs a, CsrArgs c, int cols,
+                                                          unsigned long long* sched) {
+  constexpr int GPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
+  for (;;) {
+    const int64_t i = next_item<LPR>(sched, gl, gmask);
+    if (i >= a.n_items) break;
+    csr_item<T, LPR, ALIGNED>(a, c, load_item(a.items + i), cols, gl, gmask);
+  }
+  leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
+}
+
 template <typename K>
 int persistent_grid(K kernel, int smem, int64_t n_items, int groups_per_cta, unsigned* grid) {
   int dev = 0, sms = kNumSMs, per_sm = 1;
@@ -437,26 +535,18 @@ int launch_t(const SkinnyArgs& a, int cols, unsigned long long* sched, cudaStrea
                        (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
   constexpr int per_cta = 8 * (32 / LPR);
   unsigned grid = 0;
-  if constexpr (H == 1) {
-    using S = Skinny1Smem<T, LPR>;
-    if (a.dp > S::KC) {  // wide tiles: the generic kernel
-      auto k = aligned ? spmm_skinny_kernel<T, 1, LPR, true> : spmm_skinny_kernel<T, 1, LPR, false>;
-      int rc = persistent_grid(k, 0, a.n_items, per_cta, &grid);
-      if (rc) return rc;
-      k<<<grid, 256, 0, stream>>>(a, cols, sched);
-      RB_CUDA_TRY(cudaGetLastError());
-      return RB_OK;
-    }
-    auto k = aligned ? spmm_skinny1_kernel<T, LPR, true> : spmm_skinny1_kernel<T, LPR, false>;
-    RB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::CTA_BYTES));
-    int rc = persistent_grid(k, S::CTA_BYTES, a.n_items, per_cta, &grid);
-    if (rc) return rc;
-    k<<<grid, 256, S::CTA_BYTES, stream>>>(a, cols, sched);
-  } else {
+  using S = SkinnySmem<T, LPR>;
+  if (a.dp > S::KC) {  // wide tiles: the per-column ballot kernel
     auto k = aligned ? spmm_skinny_kernel<T, H, LPR, true> : spmm_skinny_kernel<T, H, LPR, false>;
     int rc = persistent_grid(k, 0, a.n_items, per_cta, &grid);
     if (rc) return rc;
     k<<<grid, 256, 0, stream>>>(a, cols, sched);
+  } else {
+    auto k = aligned ? spmm_skinny_staged_kernel<T, H, LPR, true> : spmm_skinny_staged_kernel<T, H, LPR, false>;
+    RB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::CTA_BYTES));
+    int rc = persistent_grid(k, S::CTA_BYTES, a.n_items, per_cta, &grid);
+    if (rc) return rc;
+    k<<<grid, 256, S::CTA_BYTES, stream>>>(a, cols, sched);
   }
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
@@ -472,7 +562,36 @@ int launch_h(const SkinnyArgs& a, int cls, int cols, unsigned long long* sched, 
   }
 }
 
+template <typename T, int LPR>
+int launch_csr_t(const SkinnyArgs& a, const CsrArgs& c, int cols, unsigned long long* sched, cudaStream_t stream) {
+  const bool aligned = ((a.ldb * (int64_t)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0) &&
+                       (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
+  unsigned grid = 0;
+  auto k = aligned ? spmm_csr_kernel<T, LPR, true> : spmm_csr_kernel<T, LPR, false>;
+  int rc = persistent_grid(k, 0, a.n_items, 8 * (32 / LPR), &grid);
+  if (rc) return rc;
+  k<<<grid, 256, 0, stream>>>(a, c, cols, sched);
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}
+
 }  // namespace
+
+int launch_csr(const SkinnyArgs& a, const CsrArgs& c, int32_t b_dtype, unsigned long long* sched,
+               cudaStream_t stream) {
+  if (a.n_items <= 0) return RB_OK;
+  const int cols = skinny_cols(b_dtype, a.N);
+  switch (b_dtype) {
+    case RB_F32: return launch_csr_t<float, 32>(a, c, cols, sched, stream);
+    case RB_BF16:
+      return a.N <= 128 ? launch_csr_t<__nv_bfloat16, 16>(a, c, cols, sched, stream)
+                        : launch_csr_t<__nv_bfloat16, 32>(a, c, cols, sched, stream);
+    case RB_F16:
+      return a.N <= 128 ? launch_csr_t<__half, 16>(a, c, cols, sched, stream)
+                        : launch_csr_t<__half, 32>(a, c, cols, sched, stream);
+    default: return fail(RB_EUNSUPPORTED, "csr SpMM: unsupported dtype");
+  }
+}
 
 int skinny_cols(int32_t b_dtype, int64_t N) {
   if (b_dtype == RB_F32) return 128;  // 32 lanes x 4

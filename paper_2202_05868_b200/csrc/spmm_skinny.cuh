@@ -37,6 +37,13 @@ struct SkinnyArgs {
   int32_t* cnt;   // split-row arrival counters (zero between launches)
 };
 
+// CSR operand of the comparator kernel (spmm_csr): the reference's CsrMatrix arrays on the device.
+struct CsrArgs {
+  const int64_t* row_ptr;
+  const int64_t* col_idx;
+  const double* values;
+};
+
 // Height classes: block rows with h <= 1, 2, 4, 8 run the instance with H = 1, 2, 4, 8.
 constexpr int SKINNY_CLASSES = 4;
 constexpr int SKINNY_PART_BLOCKS = 256;  // blocks per part of a split block row
@@ -55,5 +62,10 @@ void skinny_items_for_row(int32_t g, int h, int32_t blk_begin, int nb, int64_t N
 // Launches the class-`cls` kernel over a.items[0 .. a.n_items) (persistent grid; `sched` = two
 // zero-initialised device counters owned by the plan, reset by the kernel itself on exit).
 int launch_skinny(const SkinnyArgs& a, int32_t b_dtype, int cls, unsigned long long* sched, cudaStream_t stream);
+
+// CSR comparator: items are (row, C-column slab, nonzero range relative to row_ptr[row]); a.row_perm
+// must be null (C rows = A rows).
+int launch_csr(const SkinnyArgs& a, const CsrArgs& c, int32_t b_dtype, unsigned long long* sched,
+               cudaStream_t stream);
 
 }  // namespace rb

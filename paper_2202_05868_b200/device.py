@@ -65,6 +65,49 @@ class DeviceCsr:
         vals = host_tensor(np.asarray(A.values, dtype=np.float64)).to(dev)
         return cls(A.n_rows, A.n_cols, _i64(A.row_ptr, dev), _i64(A.col_idx, dev), vals)
 
+    # ---------------------------------------------------------------- spmm_csr comparator (rb_csr_*)
+    def csr_plan(self, N: int, precision="bf16", stream=None):
+        td = L.PRECISION[precision] if isinstance(precision, str) else int(precision)
+        plans = self.__dict__.setdefault("_csr_plans", {})
+        key = (int(N), td)
+        if key not in plans:
+            h = ctypes.c_void_p(0)
+            L.check(L.lib().rb_csr_plan_create(self.n_rows, self.n_cols, L.ptr(self.row_ptr), int(N), td,
+                                               ctypes.byref(h), L.stream_handle(stream)))
+            plans[key] = h
+            weakref.finalize(self, DeviceCsr._destroy_csr_plans, plans)
+        return plans[key]
+
+    @staticmethod
+    def _destroy_csr_plans(plans):
+        try:
+            lib = L.lib()
+        except Exception:  # interpreter shutdown
+            return
+        for h in plans.values():
+            lib.rb_csr_plan_destroy(h)
+        plans.clear()
+
+    def spmm(self, B: torch.Tensor, out: torch.Tensor | None = None, precision: str | None = None,
+             stream=None) -> torch.Tensor:
+        """C[n_rows, N] (float32) = A @ B straight from CSR (spmm_csr, multiply.py:51-69)."""
+        if B.dim() != 2 or B.shape[0] != self.n_cols:
+            raise ValueError(f"dimension mismatch: {self.n_cols} vs {B.shape[0] if B.dim() == 2 else B.shape}")
+        prec = precision or {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}[B.dtype]
+        if L.TORCH_DTYPE[L.PRECISION[prec]] != B.dtype or B.stride(1) != 1:
+            raise ValueError("B must be row-major with the precision's dtype")
+        N = B.shape[1]
+        if out is None:
+            out = torch.empty((self.n_rows, N), dtype=torch.float32, device=B.device)
+        if out.dtype != torch.float32 or out.shape != (self.n_rows, N) or out.stride(1) != 1:
+            raise ValueError("out must be float32 [n_rows, N], row-major")
+        if N == 0 or self.n_rows == 0:
+            return out
+        h = self.csr_plan(N, prec, stream)
+        L.check(L.lib().rb_csr_execute(h, L.ptr(self.row_ptr), L.ptr(self.col_idx), L.ptr(self.values), L.ptr(B),
+                                       B.stride(0), L.ptr(out), out.stride(0), L.stream_handle(stream)))
+        return out
+
 
 def _boundaries(partition, n_cols: int, device) -> tuple[torch.Tensor, np.ndarray]:
     b = np.asarray(partition.boundaries if hasattr(partition, "boundaries") else partition, dtype=np.int64)

@@ -18,7 +18,8 @@ from .device import host_tensor
 from .types import DenseMatrix
 from .vbr import device_vbr_of
 
-__all__ = ["spmm_vbr", "spmm_vbr_many", "spmm_vbr_device", "upload_dense", "SpmmPipeline", "pinned_dense"]
+__all__ = ["spmm_vbr", "spmm_vbr_many", "spmm_vbr_device", "spmm_csr", "upload_dense", "SpmmPipeline",
+           "pinned_dense"]
 
 
 def upload_dense(B, precision: str, device=None) -> torch.Tensor:
@@ -38,6 +39,24 @@ def spmm_vbr_device(V, B: torch.Tensor, out=None, precision=None) -> torch.Tenso
     """Torch-native entry: V (our VbrMatrix or DeviceVbr), B device tensor → fp32 device C."""
     dv = V if hasattr(V, "spmm") else device_vbr_of(V)
     return dv.spmm(B, out=out, precision=precision)
+
+
+def spmm_csr(A, B, threads: int = 1, *, precision: str | None = None) -> DenseMatrix:
+    """Sparse-baseline product straight from CSR (multiply.py:51-69) on the GPU (csrc/csr.cu), the
+    comparator the paper measures VBR against; float64 DenseMatrix result, empty rows exact 0."""
+    from .device import DeviceCsr
+
+    if A.n_cols != B.n_rows:
+        raise ValueError(f"dimension mismatch: {A.n_cols} vs {B.n_rows}")
+    prec = precision or config.default_precision()
+    N = B.n_cols
+    if A.n_rows == 0 or N == 0:
+        return DenseMatrix(A.n_rows, N, np.zeros((A.n_rows, N)))
+    dA = A if isinstance(A, DeviceCsr) else DeviceCsr.from_host(A)
+    C32 = dA.spmm(upload_dense(B, prec), precision=prec)
+    C64 = torch.empty((A.n_rows, N), dtype=torch.float64, device=C32.device)
+    L.check(L.lib().rb_widen_f32(L.ptr(C32), A.n_rows, N, N, L.ptr(C64), N, L.stream_handle()))
+    return DenseMatrix(A.n_rows, N, C64.cpu().numpy())
 
 
 def spmm_vbr(V, B, threads: int = 1, *, precision: str | None = None) -> DenseMatrix:
