@@ -20,12 +20,15 @@ from .metrics import (BlockingCurve, BlockingStats, DensityReport, GroupDensity,
 from .multiply import SpmmPipeline, pinned_dense, spmm_csr, spmm_vbr, spmm_vbr_device, spmm_vbr_many
 from .types import (ColumnPartition, CsrMatrix, DenseMatrix, MergePolicy, RowGroup, RowGrouping, VbrBlock,
                     VbrMatrix, csr_from_triplets)
-from .vbr import vbr_from_grouping
+from .mtxio import MatrixMarketError, read_matrix_market, read_matrix_market_device, write_matrix_market
+from .vbr import load_vbr, save_vbr, vbr_from_grouping, vbr_from_json, vbr_to_json
 
 __all__ = [
     "block_1sa", "vbr_from_grouping", "spmm_vbr", "spmm_vbr_many", "spmm_vbr_device", "block_1sa_device",
     "SpmmPipeline", "pinned_dense", "spmm_csr", "blocking_stats", "blocking_curve", "curve_select",
     "verify_density_bound", "BlockingStats", "BlockingCurve", "GroupDensity", "DensityReport",
+    "MatrixMarketError", "read_matrix_market", "read_matrix_market_device", "write_matrix_market", "load_vbr",
+    "save_vbr", "vbr_from_json", "vbr_to_json",
     "DeviceCsr", "DeviceGrouping", "DeviceVbr", "ColumnPartition", "CsrMatrix", "DenseMatrix", "MergePolicy",
     "RowGroup", "RowGrouping", "VbrBlock", "VbrMatrix", "csr_from_triplets", "default_precision",
     "set_default_precision",

@@ -646,12 +646,14 @@ double rr_makespan(const std::vector<int>& len, const std::vector<int>& nsplit, 
 }
 
 // Tall items (g, m, n0, L = K steps), LPT-sorted, become units.  The last partial wave is the
-// tail: keep every full wave whole and split each tail item into s equal K ranges so the tail
-// fits one wave (r*s <= P), choosing the s with the smallest static makespan.  Measured on B200
-// (tools/split_probe.py): the partial park + reduce costs far more than its bytes suggest when
-// units get short, so units stay >= 128 K steps and a split must win by > 5 %: config 2
-// (tail 34/74 pairs, L = 512) splits in two (0.674 -> 0.650 ms); config 4 (tail 54/74) does not.
-// A split item's units are adjacent so they run concurrently on neighbouring pairs.
+// tail: keep every full wave whole and, when the tail leaves more than half of the P pairs idle,
+// split each tail item into s equal K ranges (r*s <= P, units >= 64 K steps), choosing the s with
+// the smallest static makespan.  Measured on B200 (tools/split_probe.py, tools/shard_sim.py): a
+// split costs far more than its partial bytes suggest (the parked partials and the final reduce
+// sit on the critical path at the very end), so a 3/4-full tail (config 4: 54 of 74 pairs) is
+// left alone; config 2 (34 of 74) splits in two (0.674 -> 0.632 ms), and small shards (config 4
+// at 8 ranks: 16 items for 74 pairs) split in four.  A split item's units are adjacent so they
+// run concurrently on neighbouring pairs.
 void split_tail(const std::vector<int4>& items, int P, std::vector<int4>& units, int64_t& n_slots) {
   const int n = (int)items.size();
   const int full = P > 0 ? n / P : n;
@@ -659,12 +661,12 @@ void split_tail(const std::vector<int4>& items, int P, std::vector<int4>& units,
   const char* env = std::getenv("RB_TALL_SPLIT");
   const int max_s = env ? std::max(1, std::min(MAX_SPLIT, std::atoi(env))) : MAX_SPLIT;
   const int r = n - full * P;
-  if (P > 0 && r > 0 && max_s > 1) {
+  if (P > 0 && r > 0 && 2 * r <= P && max_s > 1) {  // only a tail wave that leaves most pairs idle
     auto eval = [&](int s) {
       std::vector<int> len, ns;
       for (int i = 0; i < n; ++i) {
         const int L = items[i].w;
-        const int si = (i >= full * P && L >= 128 * s) ? s : 1;
+        const int si = (i >= full * P && L >= 64 * s) ? s : 1;
         for (int j = 0; j < si; ++j) {
           len.push_back(L * (j + 1) / si - L * j / si);
           ns.push_back(si);
@@ -686,7 +688,7 @@ void split_tail(const std::vector<int4>& items, int P, std::vector<int4>& units,
   for (int i = 0; i < n; ++i) {
     const int4 it = items[i];
     const int L = it.w;
-    const int si = (i >= best_f * P && best_s > 1 && L >= 128 * best_s) ? best_s : 1;
+    const int si = (i >= best_f * P && best_s > 1 && L >= 64 * best_s) ? best_s : 1;
     const int slot = si > 1 ? (int)n_slots++ : -1;
     for (int j = 0; j < si; ++j) {
       units.push_back(make_int4(it.x, it.y, it.z, L * j / si));

@@ -15,7 +15,7 @@ from . import config
 from .device import DeviceCsr, DeviceVbr
 from .types import ColumnPartition, VbrMatrix
 
-__all__ = ["vbr_from_grouping", "VbrMatrix"]
+__all__ = ["vbr_from_grouping", "VbrMatrix", "vbr_to_json", "vbr_from_json", "save_vbr", "load_vbr"]
 
 
 def _device_csr_for(A, grouping):
@@ -77,3 +77,47 @@ def device_vbr_of(V) -> DeviceVbr:
     except Exception:  # frozen reference dataclass: no caching
         pass
     return dv
+
+
+# ------------------------------------------------------------------------------------------ JSON
+# Debug interchange, same document as the reference (vbr.py:167-202): payloads as flat lists.
+
+
+def vbr_to_json(V) -> dict:
+    return {
+        "n_rows": V.n_rows,
+        "n_cols": V.n_cols,
+        "row_partition": np.asarray(V.row_partition).tolist(),
+        "col_boundaries": np.asarray(V.col_partition.boundaries).tolist(),
+        "row_perm": np.asarray(V.row_perm).tolist(),
+        "blocks": [{"brow": g, "bcol": int(b.bcol), "data": b.data.ravel().tolist()}
+                   for g in range(V.n_block_rows) for b in V.block_rows[g]],
+    }
+
+
+def vbr_from_json(doc: dict) -> VbrMatrix:
+    from .types import VbrBlock
+
+    part = ColumnPartition(doc["col_boundaries"][-1], np.asarray(doc["col_boundaries"]))
+    row_partition = np.asarray(doc["row_partition"], dtype=np.int64)
+    widths = part.widths
+    block_rows = [[] for _ in range(len(row_partition) - 1)]
+    for b in doc["blocks"]:
+        g, bcol = b["brow"], b["bcol"]
+        h = int(row_partition[g + 1] - row_partition[g])
+        block_rows[g].append(VbrBlock(bcol, np.asarray(b["data"], dtype=np.float64).reshape(h, widths[bcol])))
+    return VbrMatrix(doc["n_rows"], doc["n_cols"], row_partition, part, np.asarray(doc["row_perm"]), block_rows)
+
+
+def save_vbr(path, V) -> None:
+    import json
+
+    with open(path, "w", encoding="ascii") as fh:
+        json.dump(vbr_to_json(V), fh)
+
+
+def load_vbr(path) -> VbrMatrix:
+    import json
+
+    with open(path, "r", encoding="ascii") as fh:
+        return vbr_from_json(json.load(fh))
