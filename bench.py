@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=30)
     return p.parse_args()
 
 
@@ -381,7 +381,7 @@ def run_e2e(args, dv, dA, B, prec, rank, world):
     pipe = SpmmPipeline(dv, N, prec)
     if world > 1:  # each rank runs its own shard of every product
         pipe.dv = _ShardView(dv, rank, world)
-    for k in range(2):
+    for k in range(4):
         pipe.step(k, B_host[k % 2], C_host[k % 2])
     pipe.synchronize()
     torch.cuda.synchronize()
