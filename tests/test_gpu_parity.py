@@ -456,3 +456,26 @@ def test_spmm_csr_hub_rows_and_determinism(precision, N):
     torch.cuda.synchronize()
     assert torch.equal(C1, C2)
     assert np.array_equal(C1.double().cpu().numpy(), C)
+
+
+def test_edge_shapes_through_the_drop_in():
+    """Degenerate inputs behave as in the reference: an all-zero matrix (every row its own empty
+    block row or one empty group), zero dense columns, a single column / single row, a partition
+    wider than the matrix."""
+    z = rb.CsrMatrix(5, 7, np.zeros(6, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    q = rb.ColumnPartition.uniform(7, 3)
+    g = rb.block_1sa(z, q, rb.MergePolicy(tau=0.5))
+    assert g.n_groups == 1 and list(g.groups[0].rows) == [0, 1, 2, 3, 4]  # empty rows group together
+    V = rb.vbr_from_grouping(z, g, q)
+    assert V.n_stored_blocks == 0 and V.stored_area == 0
+    for prec in ("bf16", "fp32"):
+        C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(np.ones((7, 4))), precision=prec).data
+        assert C.shape == (5, 4) and np.all(C == 0.0)
+        assert rb.spmm_vbr(V, rb.DenseMatrix.from_array(np.ones((7, 0))), precision=prec).data.shape == (5, 0)
+        assert np.all(rb.spmm_csr(z, rb.DenseMatrix.from_array(np.ones((7, 3))), precision=prec).data == 0.0)
+    one = rb.CsrMatrix(1, 1, np.array([0, 1]), np.array([0]), np.array([0.5]))
+    q1 = rb.ColumnPartition.uniform(1, 64)  # partition wider than the matrix: one ragged segment
+    V1 = rb.vbr_from_grouping(one, rb.block_1sa(one, q1, rb.MergePolicy(tau=0.9)), q1)
+    for prec in ("bf16", "fp32"):
+        C = rb.spmm_vbr(V1, rb.DenseMatrix.from_array(np.array([[2.0, -4.0, 8.0]])), precision=prec).data
+        assert np.array_equal(C, np.array([[1.0, -2.0, 4.0]]))
