@@ -532,6 +532,27 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, co
 }
 
 // ------------------------------------------------------------------------------------------
+// Rows of block rows without stored blocks: C[row_perm[pos], 0:N] = 0, one warp per row, float4
+// stores (multiply.py:85-86 leaves them exactly 0).
+__global__ void __launch_bounds__(256) zero_rows_kernel(const int32_t* __restrict__ pos, int64_t n,
+                                                        const int32_t* __restrict__ row_perm, float* C, int64_t ldc,
+                                                        int32_t N) {
+  const int lane = threadIdx.x & 31;
+  const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float* dst = C + (int64_t)row_perm[pos[w]] * ldc;
+    if (vec) {
+      const int n4 = N >> 2;
+      for (int c = lane; c < n4; c += 32) reinterpret_cast<float4*>(dst)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = (n4 << 2) + lane; c < N; c += 32) dst[c] = 0.f;
+    } else {
+      for (int c = lane; c < N; c += 32) dst[c] = 0.f;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // host side
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -625,6 +646,8 @@ struct rb_spmm_plan {
   int32_t short_ns = rb::SHORT_NS;
   int64_t n_tall = 0, n_short = 0, n_simt = 0;
   rb::SkinnyItem* d_skinny = nullptr;  // skinny items, grouped by height class
+  int32_t* d_zero = nullptr;            // permuted positions of rows in block rows without blocks
+  int64_t n_zero = 0;
   float* d_skinny_ws = nullptr;     // partials of split skinny block rows
   int32_t* d_skinny_cnt = nullptr;
   unsigned long long* d_sched = nullptr;  // 2 work counters per skinny height class
@@ -748,12 +771,18 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   if (const char* sk = std::getenv("RB_SKINNY_H")) skinny_h = std::max(0, std::min(8, std::atoi(sk)));
   const int sk_cols = skinny_cols(b_dtype, N);
   std::vector<SkinnyItem> skinny[SKINNY_CLASSES];
+  std::vector<int32_t> zero_rows;  // permuted positions of the rows of empty block rows
   int64_t sk_slots = 0, sk_units = 0;
   std::vector<int32_t> short_rows;
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
     if (h <= 0 || rp[g + 1] <= row_lo || rp[g] >= row_hi) continue;
+    if (nb == 0) {  // no stored blocks: C rows are exact zeros (multiply.py:85-86), one coalesced pass
+      for (int64_t i = std::max<int64_t>(rp[g], row_lo); i < std::min<int64_t>(rp[g + 1], row_hi); ++i)
+        zero_rows.push_back((int32_t)i);
+      continue;
+    }
     if (h <= skinny_h) {
       skinny_items_for_row((int32_t)g, h, bp[g], nb, N, sk_cols, skinny[skinny_class(h)], sk_slots, sk_units);
       exec_flops += 2.0 * nb * h * (double)vbr->dp * N;
@@ -874,12 +903,24 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       return rc;
     }
   }
+  if (!zero_rows.empty()) {
+    p->n_zero = (int64_t)zero_rows.size();
+    cudaError_t e = cudaMalloc(&p->d_zero, sizeof(int32_t) * zero_rows.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_zero, zero_rows.data(), sizeof(int32_t) * zero_rows.size(), cudaMemcpyHostToDevice,
+                          stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "zero-row list");
+    }
+  }
   p->info.n_items_tall = p->n_tall;
   p->info.n_items_short = p->n_short;
   p->info.n_items_simt = p->n_simt;
   p->info.n_items_skinny = p->skinny_off[SKINNY_CLASSES];
   p->info.core_vbr_flops = core_vbr_flops;
-  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0);
+  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0);
   for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   p->info.executed_flops = exec_flops;
   p->info.vbr_flops = vbr_flops;
@@ -903,6 +944,7 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_skinny_ws) cudaFree(p->d_skinny_ws);
   if (p->d_skinny_cnt) cudaFree(p->d_skinny_cnt);
   if (p->d_sched) cudaFree(p->d_sched);
+  if (p->d_zero) cudaFree(p->d_zero);
   delete p;
   return RB_OK;
 }
@@ -929,6 +971,11 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.short_ns = p->short_ns;
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
+  if (p->n_zero > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
+    zero_rows_kernel<<<grid, 256, 0, stream>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc, (int32_t)p->N);
+    RB_CUDA_TRY(cudaGetLastError());
+  }
   if (p->skinny_off[SKINNY_CLASSES] > 0) {
     SkinnyArgs k;
     k.row_partition = p->v.row_partition;
