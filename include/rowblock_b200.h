@@ -155,6 +155,34 @@ int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t 
 int rb_spmm_plan_info(const rb_spmm_plan* plan, rb_spmm_info* info);
 int rb_spmm_execute(const rb_spmm_plan* plan, const void* B, int64_t ldb, float* C, int64_t ldc, void* stream);
 int rb_spmm_plan_destroy(rb_spmm_plan* plan);
+/* 2:4 sparse tensor-core form of the tall block rows (sparse24.cu): stage = 128 logical K of a
+ * block row's padded block sequence; 64 compressed values + 4 TMEM metadata words per tile row and
+ * stage; groups of 4 with more than two nonzeros spill into a residual CSR over permuted rows.
+ *   rb_sparse24_layout       HOST sp_tile_row[H] (-1: not tall), total compressed rows, tall count
+ *   rb_sparse24_workspace_size / rb_sparse24_emit   residual counts (res_ptr, device) and, given
+ *                            buffers, the compressed tiles [total x 64], metadata [total x 4] u32,
+ *                            residual columns (global) / values (float)
+ *   rb_spmm_plan_attach_sparse24   switches a bf16/fp16 plan's tall rows to tcgen05.mma.sp plus the
+ *                            residual pass (C += R·B).                                          */
+typedef struct rb_sparse24_device {
+  const void* sp_tiles;
+  const uint32_t* sp_meta;
+  const int64_t* sp_tile_row;   /* [H] device */
+  int64_t total_sp_rows;
+  const int64_t* res_ptr;       /* [n_rows + 1] device, permuted rows */
+  const int32_t* res_col;
+  const float* res_val;
+  int64_t n_residuals;
+} rb_sparse24_device;
+int rb_sparse24_layout(const rb_vbr_device* vbr, int64_t* sp_tile_row_host, int64_t* total_sp_rows, int64_t* n_tall,
+                       void* stream);
+int rb_sparse24_workspace_size(int64_t n_rows, int64_t total_sp_rows, size_t* bytes);
+int rb_sparse24_emit(const rb_vbr_device* vbr, const int64_t* sp_tile_row, const int32_t* tall_g,
+                     const int64_t* thread_base, int32_t n_tall, int64_t total_threads, int64_t total_sp_rows,
+                     void* workspace, size_t workspace_bytes, void* sp_tiles, uint32_t* sp_meta, int64_t* res_ptr,
+                     int32_t* res_col, float* res_val, int64_t res_capacity, int64_t* n_residuals, void* stream);
+int rb_spmm_plan_attach_sparse24(rb_spmm_plan* plan, const rb_sparse24_device* sp, void* stream);
+
 /* Host-only shard planner (no device access): the contiguous range [*row_begin, *row_end) of
  * PERMUTED row positions owned by `shard`, given HOST copies of row_partition / blk_ptr.
  * rb_spmm_plan_create(..., shard, n_shards, ...) uses exactly this range; C rows

@@ -19,7 +19,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "librowblock_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["capi.cu", "spmm.cu", "spmm_skinny.cu", "vbr_build.cu", "blocking.cu", "stats.cu", "csr.cu"]
+SOURCES = ["capi.cu", "spmm.cu", "spmm_skinny.cu", "vbr_build.cu", "blocking.cu", "stats.cu", "csr.cu", "sparse24.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
 

@@ -39,6 +39,13 @@ class VbrDevice(ctypes.Structure):
     ]
 
 
+class Sparse24Device(ctypes.Structure):
+    """Mirror of ``rb_sparse24_device``."""
+
+    _fields_ = [("sp_tiles", P), ("sp_meta", P), ("sp_tile_row", P), ("total_sp_rows", I64), ("res_ptr", P),
+                ("res_col", P), ("res_val", P), ("n_residuals", I64)]
+
+
 class SpmmInfo(ctypes.Structure):
     _fields_ = [("n_items_tall", I64), ("n_items_short", I64), ("n_items_simt", I64),
                 ("executed_flops", ctypes.c_double), ("vbr_flops", ctypes.c_double), ("row_begin_perm", I64),
@@ -78,6 +85,14 @@ def lib():
         L.rb_csr_plan_create.argtypes = [I64, I64, P, I64, I32, ctypes.POINTER(P), P]
         L.rb_csr_execute.argtypes = [P, P, P, P, P, I64, P, I64, P]
         L.rb_csr_plan_destroy.argtypes = [P]
+        L.rb_sparse24_layout.argtypes = [ctypes.POINTER(VbrDevice), P, ctypes.POINTER(I64), ctypes.POINTER(I64), P]
+        L.rb_sparse24_workspace_size.argtypes = [I64, I64, ctypes.POINTER(SZ)]
+        L.rb_sparse24_emit.argtypes = [ctypes.POINTER(VbrDevice), P, P, P, I32, I64, I64, P, SZ, P, P, P, P, P, I64,
+                                       ctypes.POINTER(I64), P]
+        L.rb_spmm_plan_attach_sparse24.argtypes = [P, ctypes.POINTER(Sparse24Device), P]
+        for name in ("rb_sparse24_layout", "rb_sparse24_workspace_size", "rb_sparse24_emit",
+                     "rb_spmm_plan_attach_sparse24"):
+            getattr(L, name).restype = INT
         for name in ("rb_csr_plan_create", "rb_csr_execute", "rb_csr_plan_destroy"):
             getattr(L, name).restype = INT
         for name in ("rb_block_1sa_workspace_size", "rb_block_1sa", "rb_vbr_workspace_size", "rb_vbr_plan",

@@ -18,3 +18,17 @@ def set_default_precision(p: str) -> None:
     if p not in ("bf16", "fp16", "fp32"):
         raise ValueError(f"unknown precision {p!r}")
     _PRECISION = p
+
+
+_SPARSE24 = os.environ.get("ROWBLOCK_B200_SPARSE24", "0") not in ("", "0", "false", "no")
+
+
+def default_sparse24() -> bool:
+    """Whether bf16/fp16 SpMM plans run the tall block rows on the 2:4 sparse tensor cores
+    (tcgen05.mma.sp over the compressed tiles + residual pass) instead of the dense tiles."""
+    return _SPARSE24
+
+
+def set_default_sparse24(on: bool) -> None:
+    global _SPARSE24
+    _SPARSE24 = bool(on)

@@ -111,6 +111,6 @@ extern "C" int rb_csr_execute(const rb_csr_plan* p, const int64_t* row_ptr, cons
   a.N = (int32_t)p->N;
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
-  CsrArgs c{row_ptr, col_idx, values};
+  CsrArgs c{row_ptr, col_idx, values, nullptr, nullptr};
   return launch_csr(a, c, p->b_dtype, p->d_sched, stream);
 }

@@ -74,6 +74,8 @@ struct SpmmArgs {
   int32_t short_ns;        // C columns per short item: 128 or 256
   float* ws;               // split-K partials of tall units: [slot][split][8 warps][8 chunks][32 cols][32 lanes]
   int32_t* cnt;            // split-K arrival counters: [slot][8 warps] (zero between launches)
+  const uint32_t* sp_meta;     // 2:4 path: TMEM metadata words (sparse24.cu layout)
+  const int64_t* sp_tile_row;  // 2:4 path: first compressed row of each tall block row
 };
 
 // Tall work unit = two int4: (g, m, n0, k0) and (k1, split, n_splits, slot).  Units with
@@ -335,6 +337,265 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// tall block rows on the 2:4 sparse tensor cores (tcgen05.mma.sp, cta_group::2, M=256 N=256 K=32
+// logical per MMA).  A stage = 128 logical K of the block row's padded block sequence: this CTA's
+// 128 compressed A rows (64 values, one SW128 TMA box of the sparse24.cu layout) + the 128 x 128
+// B panel half (four 64x64 boxes: K sub-ranges of 64 each inside one block) + 4 TMEM metadata
+// columns written by four metadata warps with tcgen05.st.  Single 256-column accumulator (TMEM
+// also holds the metadata ring), epilogue as the dense kernel.  The groups' extra nonzeros (more
+// than 2 of 4) are added by the residual pass after this kernel.
+constexpr int SP_STAGES = 4;
+constexpr int SP_THREADS = 320;  // warp 0 TMA, 1 MMA, 2-5 epilogue, 6-9 metadata
+constexpr uint32_t SP_A_BYTES = 128 * 128;
+constexpr uint32_t SP_B_BYTES = 4 * BOX_BYTES;
+constexpr uint32_t SP_STAGE_BYTES = SP_A_BYTES + SP_B_BYTES;  // 48 KB
+constexpr uint32_t SP_META_BYTES = 128 * 16;  // this CTA's 128 lanes x 4 metadata words per stage
+constexpr uint32_t SMEM_SP = SP_STAGES * (SP_STAGE_BYTES + SP_META_BYTES) + 1024 + 512;
+constexpr uint32_t SP_META_COL = 256;  // TMEM column of the metadata ring: + 16 * stage + 4 * j
+
+__device__ __forceinline__ void umma_sp_2sm(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t e_tmem,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%5], %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(e_tmem)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
+    spmm_tall2_sp_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmE, SpmmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* smeta = smem + SP_STAGES * SP_STAGE_BYTES;  // [stage][128 lanes][16 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smeta + SP_STAGES * SP_META_BYTES);
+  uint64_t* empty = full + SP_STAGES;
+  uint64_t* mfull = empty + SP_STAGES;
+  uint64_t* mload = mfull + SP_STAGES;  // per-CTA: this CTA's metadata rows landed (local TMA)
+  uint64_t* tfull = mload + SP_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SP_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&mfull[s], 8);  // 4 metadata warps x 2 CTAs
+      mbar_init(&mload[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: compressed A rows + B panel half, both CTAs
+      tma_prefetch_desc(&tmS);
+      tma_prefetch_desc(&tmB);
+      tma_prefetch_desc(&tmE);
+      const uint64_t pol_a = policy_evict_normal();
+      const uint64_t pol_b = policy_evict_last();
+      PipeState ps;
+      for (int i = pair; i < a.n_items; i += n_pairs) {
+        const int4 it = a.items[2 * i], iu = a.items[2 * i + 1];
+        const int g = it.x, m = it.y, n0 = it.z;
+        const int h = a.row_partition[g + 1] - a.row_partition[g];
+        const int hs = (h + 255) / 256 * 256;
+        const int b_begin = a.blk_ptr[g];
+        const int nb = a.blk_ptr[g + 1] - b_begin;
+        const int64_t row0 = a.sp_tile_row[g] + (int64_t)m * PAIR_BM + rank * 128;
+        const int dp = a.dp_chunks * KCH;
+        for (int s = it.w; s < iu.x; ++s) {
+          mbar_wait(&empty[ps.s], ps.ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[ps.s], 2 * SP_STAGE_BYTES);
+          uint8_t* sA = smem + ps.s * SP_STAGE_BYTES;
+          uint8_t* sB = sA + SP_A_BYTES;
+          tma_load_2d_2sm(sA, &tmS, &full[ps.s], 0, (int32_t)(row0 + (int64_t)s * hs), pol_a);
+          // this CTA's metadata rows, local barrier (read by this CTA's metadata warps)
+          mbar_arrive_expect_tx(&mload[ps.s], SP_META_BYTES);
+          tma_load_2d(smeta + ps.s * SP_META_BYTES, &tmE, &mload[ps.s], 0, (int32_t)(row0 + (int64_t)s * hs));
+          const int nb0 = n0 + (int)rank * 128;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int k = s * 128 + 64 * u;
+            const int t = k / dp, c = k - t * dp;
+            const int krow = t < nb ? a.col_bounds[a.blk_col[b_begin + t]] + c : 0;  // past the end: A is 0
+            tma_load_2d_2sm(sB + u * 2 * BOX_BYTES, &tmB, &full[ps.s], nb0, krow, pol_b);
+            tma_load_2d_2sm(sB + u * 2 * BOX_BYTES + BOX_BYTES, &tmB, &full[ps.s], nb0 + 64, krow, pol_b);
+          }
+          ps.advance(SP_STAGES);
+        }
+      }
+      for (int k = 0; k < SP_STAGES; ++k) {
+        mbar_wait(&empty[ps.s], ps.ph ^ 1);
+        ps.advance(SP_STAGES);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- sparse MMA issuer
+      const uint32_t idesc = idesc_f16(256, TALL_BN, a.ab_fmt, /*a_mn=*/0, /*b_mn=*/1) | (1u << 2);
+      PipeState ps;
+      uint32_t aph = 0;
+      for (int i = pair; i < a.n_items; i += n_pairs) {
+        const int k0 = a.items[2 * i].w, k1 = a.items[2 * i + 1].x;
+        if (k1 <= k0) continue;
+        mbar_wait(tempty, aph ^ 1);
+        tc_fence_after();
+        for (int s = k0; s < k1; ++s) {
+          mbar_wait(&full[ps.s], ps.ph);
+          mbar_wait(&mfull[ps.s], ps.ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + ps.s * SP_STAGE_BYTES);
+          const uint32_t b_base = a_base + SP_A_BYTES;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t ad = sdesc_sw128(a_base + j * 32, 16, 1024);  // 16 compressed values
+            const uint64_t bd = sdesc_sw128(b_base + (j >> 1) * 2 * BOX_BYTES + (j & 1) * 4096, BOX_BYTES, 1024);
+            umma_sp_2sm(tmem, ad, bd, idesc, tmem + SP_META_COL + 16 * ps.s + 4 * j, (s != k0) || j != 0);
+          }
+          umma_commit_2sm_mc(&empty[ps.s], 0x3);
+          ps.advance(SP_STAGES);
+        }
+        umma_commit_2sm_mc(tfull, 0x3);
+        aph ^= 1;
+      }
+    }
+  } else if (warp >= 6) {
+    // ---------------- metadata writers: TMEM lane quadrant of this warp, 4 words per stage
+    const int quad = warp & 3;
+    PipeState ps;
+    for (int i = pair; i < a.n_items; i += n_pairs) {
+      const int4 it = a.items[2 * i], iu = a.items[2 * i + 1];
+      for (int s = it.w; s < iu.x; ++s) {
+        mbar_wait(&mload[ps.s], ps.ph);  // implies the slot's previous MMAs are done (producer waited empty)
+        const uint4 w = *reinterpret_cast<const uint4*>(smeta + ps.s * SP_META_BYTES + (quad * 32 + lane) * 16);
+        const uint32_t col = tmem + ((uint32_t)(quad * 32) << 16) + SP_META_COL + 16 * ps.s;
+        tmem_st_32x32b_x1(col + 0, w.x);
+        tmem_st_32x32b_x1(col + 4, w.y);
+        tmem_st_32x32b_x1(col + 8, w.z);
+        tmem_st_32x32b_x1(col + 12, w.w);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&mfull[ps.s]);
+        ps.advance(SP_STAGES);
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs), single accumulator
+    const int q = warp & 3;
+    const bool vec = ((a.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
+    uint32_t aph = 0;
+    for (int i = pair; i < a.n_items; i += n_pairs) {
+      const int4 it = a.items[2 * i], iu = a.items[2 * i + 1];
+      const int g = it.x, m = it.y, n0 = it.z;
+      const int p0 = a.row_partition[g];
+      const int h = a.row_partition[g + 1] - p0;
+      const int nk = iu.x - it.w;
+      const int row_local = m * PAIR_BM + (int)rank * 128 + q * 32 + lane;
+      const bool valid = row_local < h;
+      const int64_t crow = valid ? (int64_t)a.row_perm[p0 + row_local] : 0;
+      float* dst = a.C + crow * a.ldc + n0;
+      const int ncol = min(TALL_BN, a.N - n0);
+      if (nk <= 0) continue;
+      mbar_wait(tfull, aph);
+      tc_fence_after();
+      if (iu.z > 1) {
+        const int wslot = (int)rank * 4 + q;
+        float* part = a.ws + ((size_t)iu.w * MAX_SPLIT + iu.y) * 8 * WARP_PART + (size_t)wslot * WARP_PART;
+        float4* part4 = reinterpret_cast<float4*>(part);
+        for (int c = 0; c < ncol; c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(part4 + (c >> 5) * 256 + j * 32 + lane,
+                   make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(tempty);
+        aph ^= 1;
+        __threadfence();
+        __syncwarp();
+        int old = 0;
+        int* ctr = a.cnt + iu.w * 8 + wslot;
+        if (lane == 0) old = atomicAdd(ctr, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == iu.z - 1) {
+          __threadfence();
+          const float4* base4 = reinterpret_cast<const float4*>(a.ws + (size_t)iu.w * MAX_SPLIT * 8 * WARP_PART +
+                                                                (size_t)wslot * WARP_PART);
+          constexpr int SPLIT_STRIDE4 = 8 * WARP_PART / 4;
+          for (int c = 0; c < ncol; c += 32) {
+            float4 v[MAX_SPLIT][8];
+#pragma unroll
+            for (int sp = 0; sp < MAX_SPLIT; ++sp)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                v[sp][j] = sp < iu.z ? __ldcg(base4 + sp * SPLIT_STRIDE4 + (c >> 5) * 256 + j * 32 + lane)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t r[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 t = v[0][j];
+#pragma unroll
+              for (int sp = 1; sp < MAX_SPLIT; ++sp)
+                if (sp < iu.z) {
+                  t.x += v[sp][j].x;
+                  t.y += v[sp][j].y;
+                  t.z += v[sp][j].z;
+                  t.w += v[sp][j].w;
+                }
+              r[4 * j] = __float_as_uint(t.x);
+              r[4 * j + 1] = __float_as_uint(t.y);
+              r[4 * j + 2] = __float_as_uint(t.z);
+              r[4 * j + 3] = __float_as_uint(t.w);
+            }
+            if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+          }
+          if (lane == 0) *ctr = 0;
+        }
+        continue;
+      }
+      for (int c = 0; c < ncol; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+        tmem_ld_wait();
+        if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(tempty);
+      aph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_2sm<512>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------
 // short block rows (swap-AB), one CTA.  Item = (g, hp, n0).  D_mt^T[128 C cols x hp rows] at TMEM
 // columns acc*256 + mt*hp.
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -568,7 +829,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
-                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(RB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(RB_EINVAL, "TMA base must be 16-byte aligned");
@@ -578,7 +840,7 @@ static int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(RB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return RB_OK;
 }
@@ -648,6 +910,19 @@ struct rb_spmm_plan {
   rb::SkinnyItem* d_skinny = nullptr;  // skinny items, grouped by height class
   int32_t* d_zero = nullptr;            // permuted positions of rows in block rows without blocks
   int64_t n_zero = 0;
+  std::vector<int4> tall_items;         // (g, m, n0, -) before K splitting (for the 2:4 re-plan)
+  int64_t shard_lo = 0, shard_hi = 0;
+  // 2:4 sparse path (rb_spmm_plan_attach_sparse24)
+  bool use_sp = false;
+  rb_sparse24_device sp{};
+  CUtensorMap tmSP, tmSPE;
+  int4* d_sp_units = nullptr;
+  int64_t n_sp_units = 0;
+  float* d_sp_ws = nullptr;
+  int32_t* d_sp_cnt = nullptr;
+  rb::SkinnyItem* d_res_items = nullptr;
+  int64_t n_res_items = 0;
+  unsigned long long* d_res_sched = nullptr;
   float* d_skinny_ws = nullptr;     // partials of split skinny block rows
   int32_t* d_skinny_cnt = nullptr;
   unsigned long long* d_sched = nullptr;  // 2 work counters per skinny height class
@@ -833,6 +1108,9 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   p->b_dtype = b_dtype;
   p->short_ns = short_ns;
   p->n_tall = (int64_t)tall_units.size() / 2;
+  p->tall_items = tall;
+  p->shard_lo = row_lo;
+  p->shard_hi = row_hi;
   p->n_split_slots = n_slots;
   p->n_short = (int64_t)shrt.size();
   p->n_simt = (int64_t)simt.size();
@@ -929,6 +1207,90 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   return RB_OK;
 }
 
+// Switch the plan's tall block rows to the 2:4 sparse tensor-core kernel over the compressed form
+// built by rb_sparse24_emit, plus the residual pass (C += residuals x B) for the groups that keep
+// more than two nonzeros.  Work units are re-planned in stages of 128 logical K.
+extern "C" int rb_spmm_plan_attach_sparse24(rb_spmm_plan* p, const rb_sparse24_device* sp, void* stream_) {
+  if (!p || !sp) return fail(RB_EINVAL, "null argument");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (p->b_dtype != RB_BF16 && p->b_dtype != RB_F16) return fail(RB_EUNSUPPORTED, "2:4 path needs bf16/fp16");
+  const int64_t H = p->v.n_block_rows, n = p->v.n_rows;
+  std::vector<int32_t> rp(H + 1), bp(H + 1);
+  std::vector<int64_t> spr(std::max<int64_t>(H, 1)), res(n + 1);
+  if (H > 0) {
+    RB_CUDA_TRY(cudaMemcpyAsync(rp.data(), p->v.row_partition, 4 * (H + 1), cudaMemcpyDeviceToHost, stream));
+    RB_CUDA_TRY(cudaMemcpyAsync(bp.data(), p->v.blk_ptr, 4 * (H + 1), cudaMemcpyDeviceToHost, stream));
+    RB_CUDA_TRY(cudaMemcpyAsync(spr.data(), sp->sp_tile_row, 8 * H, cudaMemcpyDeviceToHost, stream));
+  }
+  if (sp->n_residuals > 0)
+    RB_CUDA_TRY(cudaMemcpyAsync(res.data(), sp->res_ptr, 8 * (n + 1), cudaMemcpyDeviceToHost, stream));
+  RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  std::vector<int4> items;
+  for (const int4& it : p->tall_items) {
+    const int g = it.x;
+    if (spr[g] < 0) return fail(RB_EINVAL, "sparse form does not cover a tall block row");
+    const int64_t S = ((int64_t)(bp[g + 1] - bp[g]) * p->v.dp + 127) / 128;
+    items.push_back(make_int4(g, it.y, it.z, (int)S));
+  }
+  std::stable_sort(items.begin(), items.end(), [](const int4& x, const int4& y) { return x.w > y.w; });
+  int dev = 0, sms = kNumSMs;
+  RB_CUDA_TRY(cudaGetDevice(&dev));
+  RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::vector<int4> units;
+  int64_t n_slots = 0;
+  split_tail(items, sms / 2, units, n_slots);
+  // residual rows of this shard's tall block rows
+  const int cols = skinny_cols(p->b_dtype, p->N);
+  std::vector<SkinnyItem> ritems;
+  if (sp->n_residuals > 0)
+    for (const int4& it : p->tall_items) {
+      const int g = it.x;
+      if (it.z != 0) continue;  // one pass per pair tile: rows m*256 .. +256
+      for (int r = it.y * PAIR_BM; r < std::min(rp[g + 1] - rp[g], (it.y + 1) * PAIR_BM); ++r) {
+        const int64_t pos = rp[g] + r;
+        const int64_t c = res[pos + 1] - res[pos];
+        if (c <= 0) continue;
+        for (int64_t n0 = 0; n0 < p->N; n0 += cols)
+          ritems.push_back(SkinnyItem{(int32_t)pos, (int32_t)n0, 0, (int32_t)c, 0, 1, -1, 0});
+      }
+    }
+  cudaError_t e = cudaSuccess;
+  if (p->d_sp_units) cudaFree(p->d_sp_units);
+  p->d_sp_units = nullptr;
+  if (!units.empty()) e = cudaMalloc(&p->d_sp_units, sizeof(int4) * units.size());
+  if (e == cudaSuccess && !units.empty())
+    e = cudaMemcpyAsync(p->d_sp_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && n_slots > 0 && !p->d_sp_ws)
+    e = cudaMalloc(&p->d_sp_ws, sizeof(float) * (size_t)n_slots * MAX_SPLIT * 8 * WARP_PART);
+  if (e == cudaSuccess && n_slots > 0 && !p->d_sp_cnt) e = cudaMalloc(&p->d_sp_cnt, sizeof(int32_t) * 8 * n_slots);
+  if (e == cudaSuccess && n_slots > 0) e = cudaMemsetAsync(p->d_sp_cnt, 0, sizeof(int32_t) * 8 * n_slots, stream);
+  if (e == cudaSuccess && !ritems.empty()) e = cudaMalloc(&p->d_res_items, sizeof(SkinnyItem) * ritems.size());
+  if (e == cudaSuccess && !ritems.empty())
+    e = cudaMemcpyAsync(p->d_res_items, ritems.data(), sizeof(SkinnyItem) * ritems.size(), cudaMemcpyHostToDevice,
+                        stream);
+  if (e == cudaSuccess && !p->d_res_sched) e = cudaMalloc(&p->d_res_sched, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->d_res_sched, 0, 2 * sizeof(unsigned long long), stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, cudaGetErrorString(e));
+  if (sp->total_sp_rows > 0) {
+    const CUtensorMapDataType dt =
+        p->b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    int rc = make_tmap_2d(&p->tmSP, sp->sp_tiles, dt, 64, (uint64_t)sp->total_sp_rows, 128, 64, 128);
+    if (!rc)
+      rc = make_tmap_2d(&p->tmSPE, sp->sp_meta, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, (uint64_t)sp->total_sp_rows, 16, 4,
+                        128, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+  }
+  p->sp = *sp;
+  p->n_sp_units = (int64_t)units.size() / 2;
+  p->n_res_items = (int64_t)ritems.size();
+  p->use_sp = true;
+  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0) +
+                       (p->n_res_items > 0);
+  for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
+  return RB_OK;
+}
+
 extern "C" int rb_spmm_plan_info(const rb_spmm_plan* p, rb_spmm_info* info) {
   if (!p || !info) return fail(RB_EINVAL, "null argument");
   *info = p->info;
@@ -945,6 +1307,11 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_skinny_cnt) cudaFree(p->d_skinny_cnt);
   if (p->d_sched) cudaFree(p->d_sched);
   if (p->d_zero) cudaFree(p->d_zero);
+  if (p->d_sp_units) cudaFree(p->d_sp_units);
+  if (p->d_sp_ws) cudaFree(p->d_sp_ws);
+  if (p->d_sp_cnt) cudaFree(p->d_sp_cnt);
+  if (p->d_res_items) cudaFree(p->d_res_items);
+  if (p->d_res_sched) cudaFree(p->d_res_sched);
   delete p;
   return RB_OK;
 }
@@ -971,13 +1338,15 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.short_ns = p->short_ns;
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
+  a.sp_meta = nullptr;
+  a.sp_tile_row = nullptr;
   if (p->n_zero > 0) {
     const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
     zero_rows_kernel<<<grid, 256, 0, stream>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc, (int32_t)p->N);
     RB_CUDA_TRY(cudaGetLastError());
   }
   if (p->skinny_off[SKINNY_CLASSES] > 0) {
-    SkinnyArgs k;
+    SkinnyArgs k{};
     k.row_partition = p->v.row_partition;
     k.row_perm = p->v.row_perm;
     k.blk_ptr = p->v.blk_ptr;
@@ -1028,7 +1397,40 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   int dev = 0, sms = kNumSMs;
   RB_CUDA_TRY(cudaGetDevice(&dev));
   RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (p->n_tall > 0) {
+  if (p->n_tall > 0 && p->use_sp) {
+    static bool sp_attr = false;
+    if (!sp_attr) {
+      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
+      sp_attr = true;
+    }
+    SpmmArgs s = a;
+    s.items = p->d_sp_units;
+    s.n_items = (int32_t)p->n_sp_units;
+    s.ws = p->d_sp_ws;
+    s.cnt = p->d_sp_cnt;
+    s.sp_meta = p->sp.sp_meta;
+    s.sp_tile_row = p->sp.sp_tile_row;
+    const int pairs = (int)std::min<int64_t>(sms / 2, p->n_sp_units);
+    if (pairs > 0) {
+      spmm_tall2_sp_kernel<<<(unsigned)(2 * pairs), SP_THREADS, SMEM_SP, stream>>>(p->tmSP, tmB, p->tmSPE, s);
+      RB_CUDA_TRY(cudaGetLastError());
+    }
+    if (p->n_res_items > 0) {  // C += residuals x B (groups of 4 with more than two nonzeros)
+      SkinnyArgs k{};
+      k.row_perm = p->v.row_perm;
+      k.items = p->d_res_items;
+      k.n_items = p->n_res_items;
+      k.B = B;
+      k.ldb = ldb;
+      k.C = C;
+      k.ldc = ldc;
+      k.N = (int32_t)p->N;
+      k.accumulate = 1;
+      CsrArgs c{p->sp.res_ptr, nullptr, nullptr, p->sp.res_col, p->sp.res_val};
+      int rc = launch_csr(k, c, p->b_dtype, p->d_res_sched, stream);
+      if (rc) return rc;
+    }
+  } else if (p->n_tall > 0) {
     a.items = p->d_items;
     a.n_items = (int32_t)p->n_tall;
     const int pairs = (int)std::min<int64_t>(sms / 2, p->n_tall);

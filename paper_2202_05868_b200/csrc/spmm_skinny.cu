@@ -93,15 +93,21 @@ __device__ __forceinline__ void fma_row(float (&acc)[16 / sizeof(T)], float a, c
 }
 
 template <int VEC, bool ALIGNED>
-__device__ __forceinline__ void store_c(float* dst, int n, int N, const float (&v)[VEC]) {
+__device__ __forceinline__ void store_c(float* dst, int n, int N, const float (&v)[VEC], bool accumulate = false) {
   if (ALIGNED && n + VEC <= N) {
 #pragma unroll
-    for (int e = 0; e < VEC; e += 4)
-      *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+    for (int e = 0; e < VEC; e += 4) {
+      float4 o = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      if (accumulate) {
+        const float4 c = *reinterpret_cast<const float4*>(dst + e);
+        o = make_float4(c.x + o.x, c.y + o.y, c.z + o.z, c.w + o.w);
+      }
+      *reinterpret_cast<float4*>(dst + e) = o;
+    }
   } else {
 #pragma unroll
     for (int e = 0; e < VEC; ++e)
-      if (n + e < N) dst[e] = v[e];
+      if (n + e < N) dst[e] = accumulate ? dst[e] + v[e] : v[e];
   }
 }
 
@@ -160,7 +166,7 @@ __device__ __forceinline__ void skinny_finish(const SkinnyArgs& a, const SkinnyI
   for (int r = 0; r < H; ++r)
     if (r < h) {
       const int64_t crow = a.row_perm ? (int64_t)a.row_perm[p0 + r] : (int64_t)p0 + r;  // CSR: identity
-      store_c<VEC, ALIGNED>(a.C + crow * a.ldc + n, n, a.N, acc[r]);
+      store_c<VEC, ALIGNED>(a.C + crow * a.ldc + n, n, a.N, acc[r], a.accumulate != 0);
     }
 }
 
@@ -484,8 +490,13 @@ __device__ __forceinline__ void csr_item(const SkinnyArgs& a, const CsrArgs& c, 
     int col = 0;
     float val = 0.f;
     if (gl < cnt) {
-      col = (int)__ldg(c.col_idx + j0 + gl);
-      val = round_to<T>(__ldg(c.values + j0 + gl));  // A rounded to the operand dtype, as in VBR tiles
+      if (c.col32) {
+        col = __ldg(c.col32 + j0 + gl);
+        val = __ldg(c.val32 + j0 + gl);
+      } else {
+        col = (int)__ldg(c.col_idx + j0 + gl);
+        val = round_to<T>(__ldg(c.values + j0 + gl));  // A rounded to the operand dtype, as in VBR tiles
+      }
     }
     for (int i = 0; i < cnt; i += 8) {
       float av[8];

@@ -35,6 +35,7 @@ struct SkinnyArgs {
   int32_t N;
   float* ws;      // split-row partials
   int32_t* cnt;   // split-row arrival counters (zero between launches)
+  int32_t accumulate;  // 1: C += result (2:4 residual pass), 0: C = result
 };
 
 // CSR operand of the comparator kernel (spmm_csr): the reference's CsrMatrix arrays on the device.
@@ -42,6 +43,8 @@ struct CsrArgs {
   const int64_t* row_ptr;
   const int64_t* col_idx;
   const double* values;
+  const int32_t* col32;  // alternative operand (2:4 residuals): int32 columns, float values
+  const float* val32;
 };
 
 // Height classes: block rows with h <= 1, 2, 4, 8 run the instance with H = 1, 2, 4, 8.

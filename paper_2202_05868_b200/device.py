@@ -255,14 +255,71 @@ class DeviceVbr:
                            self.blk_ptr.data_ptr(), self.blk_col.data_ptr(), self.grp_tile_row.data_ptr(),
                            self.col_bounds.data_ptr(), t.data_ptr())
 
-    def plan(self, N: int, precision="bf16", shard: int = 0, n_shards: int = 1, stream=None):
+    # ---------------------------------------------------------------- 2:4 sparse form (rb_sparse24_*)
+    def sparse24(self, precision="bf16", stream=None) -> "L.Sparse24Device":
+        """Compressed 2:4 form of the tall block rows (+ residual CSR), built once per dtype."""
         td = L.PRECISION[precision] if isinstance(precision, str) else int(precision)
-        key = (int(N), td, int(shard), int(n_shards))
+        cache = self.__dict__.setdefault("_sp24", {})
+        if td in cache:
+            return cache[td][0]
+        lib = L.lib()
+        dev = self.blk_ptr.device
+        s = self._struct(td)
+        H = self.n_block_rows
+        spr_host = np.zeros(max(H, 1), np.int64)
+        total, n_tall = ctypes.c_int64(0), ctypes.c_int64(0)
+        L.check(lib.rb_sparse24_layout(ctypes.byref(s), ctypes.c_void_p(spr_host.ctypes.data), ctypes.byref(total),
+                                       ctypes.byref(n_tall), L.stream_handle(stream)))
+        rp = self.row_partition.cpu().numpy().astype(np.int64)
+        tall_g = np.flatnonzero(spr_host[:H] >= 0).astype(np.int32)
+        hs = ((np.diff(rp)[tall_g] + 255) // 256 * 256).astype(np.int64)
+        tbase = np.concatenate([[0], np.cumsum(hs)]).astype(np.int64)
+        keep = {
+            "sp_tile_row": torch.from_numpy(spr_host).to(dev),
+            "tall_g": torch.from_numpy(tall_g if len(tall_g) else np.zeros(1, np.int32)).to(dev),
+            "tbase": torch.from_numpy(tbase).to(dev),
+            "tiles": torch.zeros((max(total.value, 1), 64), dtype=L.TORCH_DTYPE[td], device=dev),
+            "meta": torch.zeros(max(total.value, 1) * 4, dtype=torch.int32, device=dev),
+            "res_ptr": torch.zeros(self.n_rows + 1, dtype=torch.int64, device=dev),
+        }
+        wsb = ctypes.c_size_t(0)
+        L.check(lib.rb_sparse24_workspace_size(self.n_rows, total.value, ctypes.byref(wsb)))
+        ws = torch.empty(max(1, wsb.value), dtype=torch.uint8, device=dev)
+        n_res = ctypes.c_int64(0)
+        args = lambda tiles, meta, rc, rv, cap: (  # noqa: E731
+            ctypes.byref(s), L.ptr(keep["sp_tile_row"]), L.ptr(keep["tall_g"]), L.ptr(keep["tbase"]), len(tall_g),
+            int(tbase[-1]), total.value, L.ptr(ws), wsb.value, tiles, meta, L.ptr(keep["res_ptr"]), rc, rv, cap,
+            ctypes.byref(n_res), L.stream_handle(stream))
+        L.check(lib.rb_sparse24_emit(*args(None, None, None, None, 0)))  # residual counts
+        keep["res_col"] = torch.empty(max(n_res.value, 1), dtype=torch.int32, device=dev)
+        keep["res_val"] = torch.empty(max(n_res.value, 1), dtype=torch.float32, device=dev)
+        L.check(lib.rb_sparse24_emit(*args(L.ptr(keep["tiles"]), L.ptr(keep["meta"]), L.ptr(keep["res_col"]),
+                                           L.ptr(keep["res_val"]), n_res.value)))
+        sp = L.Sparse24Device(keep["tiles"].data_ptr(), keep["meta"].data_ptr(), keep["sp_tile_row"].data_ptr(),
+                              total.value, keep["res_ptr"].data_ptr(), keep["res_col"].data_ptr(),
+                              keep["res_val"].data_ptr(), n_res.value)
+        cache[td] = (sp, keep)
+        return sp
+
+    def plan(self, N: int, precision="bf16", shard: int = 0, n_shards: int = 1, stream=None,
+             sparse24: bool | None = None):
+        from . import config
+
+        td = L.PRECISION[precision] if isinstance(precision, str) else int(precision)
+        sp24 = (config.default_sparse24() if sparse24 is None else bool(sparse24)) and td in (L.RB_BF16, L.RB_F16)
+        key = (int(N), td, int(shard), int(n_shards), sp24)
         if key not in self._plans:
             s = self._struct(td)
             h = ctypes.c_void_p(0)
             L.check(L.lib().rb_spmm_plan_create(ctypes.byref(s), int(N), td, int(shard), int(n_shards),
                                                 ctypes.byref(h), L.stream_handle(stream)))
+            if sp24:
+                try:
+                    L.check(L.lib().rb_spmm_plan_attach_sparse24(h, ctypes.byref(self.sparse24(td, stream)),
+                                                                 L.stream_handle(stream)))
+                except Exception:
+                    L.lib().rb_spmm_plan_destroy(h)
+                    raise
             self._plans[key] = h
             if self._finalizer is None:
                 self._finalizer = weakref.finalize(self, DeviceVbr._destroy_plans, self._plans)
@@ -278,13 +335,14 @@ class DeviceVbr:
             lib.rb_spmm_plan_destroy(h)
         plans.clear()
 
-    def plan_info(self, N: int, precision="bf16", shard: int = 0, n_shards: int = 1) -> dict:
+    def plan_info(self, N: int, precision="bf16", shard: int = 0, n_shards: int = 1, sparse24=None) -> dict:
         info = L.SpmmInfo()
-        L.check(L.lib().rb_spmm_plan_info(self.plan(N, precision, shard, n_shards), ctypes.byref(info)))
+        L.check(L.lib().rb_spmm_plan_info(self.plan(N, precision, shard, n_shards, sparse24=sparse24),
+                                          ctypes.byref(info)))
         return {f: getattr(info, f) for f, _ in L.SpmmInfo._fields_}
 
     def spmm(self, B: torch.Tensor, out: torch.Tensor | None = None, precision: str | None = None,
-             shard: int = 0, n_shards: int = 1, stream=None) -> torch.Tensor:
+             shard: int = 0, n_shards: int = 1, stream=None, sparse24: bool | None = None) -> torch.Tensor:
         """C[n_rows, N] (float32) = A @ B on the device.  B: [n_cols, N] bf16/fp16/fp32 (row stride
         a multiple of 8 elements for 16-bit types).  ``out`` rows not owned by ``shard`` are untouched."""
         if B.dim() != 2 or B.shape[0] != self.n_cols:
@@ -301,7 +359,7 @@ class DeviceVbr:
             raise ValueError("out must be float32 [n_rows, N], row-major")
         if N == 0 or self.n_rows == 0:
             return out
-        h = self.plan(N, prec, shard, n_shards, stream)
+        h = self.plan(N, prec, shard, n_shards, stream, sparse24=sparse24)
         L.check(L.lib().rb_spmm_execute(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0),
                                         L.stream_handle(stream)))
         return out
