@@ -25,3 +25,39 @@ def test_rmat_block_1sa_matches_pruned_oracle(scale, tau):
     pp = dg.pattern_ptr[: dg.n_groups + 1].cpu().numpy()
     assert np.array_equal(pp, ref["pattern_ptr"])
     assert np.array_equal(dg.pattern_idx[: pp[-1]].cpu().numpy(), ref["pattern_idx"])
+
+
+def _digest(t):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy().astype(np.int64)).tobytes()).hexdigest()
+
+
+def _full_cases():
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_cfg3_full.json")
+    doc = json.load(open(path))
+    return doc, sorted(k for k in doc if k != "input")
+
+
+@pytest.mark.parametrize("tau", _full_cases()[1])
+def test_rmat_full_size_block_1sa_matches_oracle_digest(tau):
+    """Config 3 at full size (R-MAT 2^20, 16M nnz; the Python reference cannot run it): the device
+    1-SA is bit-exact with the pruned C oracle (pinned to the reference on every golden case), via
+    SHA-256 digests of every output array (tests/golden/make_golden_cfg3.py)."""
+    doc, _ = _full_cases()
+    dA, bounds, cfg, meta = synth.make("3", scale=1, device="cuda")
+    assert _digest(dA.row_ptr) == doc["input"]["row_ptr"] and _digest(dA.col_idx) == doc["input"]["col_idx"]
+    dg = block_1sa_device(dA, bounds, MergePolicy(tau=float(tau)), True)
+    ref = doc[tau]
+    H = dg.n_groups
+    assert H == ref["n_groups"]
+    assert _digest(dg.group_of) == ref["group_of"]
+    assert _digest(dg.row_perm) == ref["row_perm"]
+    assert _digest(dg.group_ptr[: H + 1]) == ref["group_ptr"]
+    assert _digest(dg.seed_size[:H]) == ref["seed_size"]
+    pp = dg.pattern_ptr[: H + 1]
+    assert _digest(pp) == ref["pattern_ptr"]
+    assert _digest(dg.pattern_idx[: int(pp[-1].item())]) == ref["pattern_idx"]
