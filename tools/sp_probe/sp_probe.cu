@@ -31,7 +31,8 @@ __device__ __forceinline__ void umma_sp(uint32_t d, uint64_t a, uint64_t b, uint
 
 // A_c: [128][16] bf16 compressed (row-major), B: [32][64] bf16 (k rows, n contiguous), E: [128] u32 per lane
 __global__ void probe(const __nv_bfloat16* Ac, const __nv_bfloat16* B, const uint32_t* E, float* C, uint32_t idesc,
-                      int e_col) {
+                      int e_col, int mode) {
+  __shared__ __align__(1024) uint32_t sE[128 * 4];  // 128 lanes x 16 B, row-contiguous (cp source)
   __shared__ __align__(1024) uint8_t sA[128 * 128];  // SW128 K-major: 128 rows x 128 B (only first 32 B used)
   __shared__ __align__(1024) uint8_t sB[32 * 128];   // SW128 MN-major: 32 k-rows x 128 B (64 n)
   __shared__ uint64_t bar;
@@ -59,15 +60,30 @@ __global__ void probe(const __nv_bfloat16* Ac, const __nv_bfloat16* B, const uin
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
-  // metadata: each warp writes its 32 lanes of column e_col
-  tmem_st_32x32b_x1(tmem + ((uint32_t)(warp * 32) << 16) + e_col, E[t]);
-  tmem_st_wait();
+  // metadata: each warp writes its 32 lanes of column e_col (mode 0), or tcgen05.cp 128x128b
+  if (mode == 0) {
+    tmem_st_32x32b_x1(tmem + ((uint32_t)(warp * 32) << 16) + e_col, E[t]);
+    tmem_st_wait();
+  } else {
+    const int w = mode >= 2 ? mode - 2 : 0;  // word slot of this MMA's metadata (selected by idesc id2)
+    for (int j = 0; j < 4; ++j) sE[t * 4 + j] = j == w ? E[t] : 0xFFFFFFFFu;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (t == 0) {
     const uint64_t ad = sdesc_sw128(smem_u32(sA), 16, 1024);
     const uint64_t bd = sdesc_sw128(smem_u32(sB), 8192, 1024);
+    if (mode != 0) {
+      // no-swizzle K-major descriptor: 8-row core matrices of 16 B rows, SBO = 128 B between them
+      uint64_t ed = 0;
+      ed |= (uint64_t)((smem_u32(sE) >> 4) & 0x3FFF);
+      ed |= (uint64_t)((16 >> 4) & 0x3FFF) << 16;
+      ed |= (uint64_t)((128 >> 4) & 0x3FFF) << 32;
+      ed |= (uint64_t)1 << 46;
+      asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(tmem + e_col), "l"(ed) : "memory");
+    }
     umma_sp(tmem, ad, bd, idesc, tmem + e_col, 0);
     umma_commit(&bar);
   }
@@ -244,7 +260,7 @@ int main(int argc, char** argv) {
     for (int c = 0; c < 8; ++c) {
       const int k = 4 * c;
       uint32_t lane, bit;
-      if (variant == 0) {
+      if (variant != 1) {
         const int m0 = m & 7, m1 = (m >> 3) & 1, m2 = m >> 4, k0 = k & 15, k1 = k >> 4;
         lane = m0 + 8 * k1 + 16 * m2;
         bit = k0 + 16 * m1;
@@ -272,7 +288,14 @@ int main(int argc, char** argv) {
   cudaMemcpy(dB, Bh.data(), Bh.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dE, E.data(), 512, cudaMemcpyHostToDevice);
   const uint32_t idesc = idesc_f16(M, N, 1, 0, 1) | (1u << 2);  // sparse flag
-  probe<<<1, 128>>>(dA, dB, dE, dC, idesc, 96);
+  int mode = variant >= 3 ? 1 : 0;
+  int ecol = variant == 4 ? 97 : variant == 5 ? 98 : 96;
+  uint32_t id = idesc;
+  if (variant >= 6) {  // metadata in word (variant - 6) of the 128-bit cp, selected by sparse_id2
+    mode = 2 + (variant - 6);
+    id = idesc | (uint32_t)(variant - 6);
+  }
+  probe<<<1, 128>>>(dA, dB, dE, dC, id, ecol, variant == 4 ? 0 : mode);
   cudaError_t err = cudaDeviceSynchronize();
   printf("variant %d: %s\n", variant, cudaGetErrorString(err));
   if (err) return 1;
