@@ -160,7 +160,7 @@ int rb_spmm_plan_destroy(rb_spmm_plan* plan);
  * stage; groups of 4 with more than two nonzeros spill into a residual CSR over permuted rows.
  *   rb_sparse24_layout       HOST sp_tile_row[H] (-1: not tall), total compressed rows, tall count
  *   rb_sparse24_workspace_size / rb_sparse24_emit   residual counts (res_ptr, device) and, given
- *                            buffers, the compressed tiles [total x 64], metadata [total x 4] u32,
+ *                            buffers, the compressed tiles [total x 64], metadata [total x 8] u32,
  *                            residual columns (global) / values (float)
  *   rb_spmm_plan_attach_sparse24   switches a bf16/fp16 plan's tall rows to tcgen05.mma.sp plus the
  *                            residual pass (C += R·B).                                          */

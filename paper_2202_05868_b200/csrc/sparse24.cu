@@ -9,9 +9,11 @@
 //
 // Layout (per tall block row g, hs = roundup(h, 256) rows, S_g = ceil(nb_g * dp / 128) stages):
 //   sp_tiles [sp_tile_row[g] + s*hs + r][64]   compressed values (bf16/fp16), rows >= h are zero
-//   sp_meta  [(sp_tile_row[g] + s*hs + 128*q + L) * 4 + j]  uint32: the TMEM metadata word of lane L
-//            (of the 128-row quarter-pair q) for the j-th K=32 MMA of the stage, in the f16 sparse
-//            layout verified by tools/sp_probe: lane L = m0 + 8*k1 + 16*m2 holds rows
+//   sp_meta  [(sp_tile_row[g] + s*hs + 128*q + L) * 8 + 4*(j/2) + j%2]  uint32 (words 2,3,6,7 zero):
+//            the TMEM metadata word of lane L (of the 128-row group q) for the j-th K=32 MMA of the
+//            stage.  Two 16-byte planes per row, one tcgen05.cp 128x128b each; the MMA reads its word
+//            at a 4-column-aligned TMEM address with idesc sparse_id2 = j%2 (tools/sp_probe).
+//            Word layout (f16 sparse, verified by tools/sp_probe): lane L = m0 + 8*k1 + 16*m2 holds rows
 //            m = m0 + 8*m1 + 16*m2 (m1 = 0, 1) at bits 16*m1 + k0 for logical k = 16*k1 + k0;
 //            each 4-bit nibble = (i1 << 2) | i0, the kept positions of a group of 4.
 //   res_ptr [n_rows + 1] (permuted rows), res_col (global column), res_val (float).
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(256) sp24_rows_kernel(SpArgs a, const T* __res
 
 // Transpose chunk-ordered nibbles into TMEM lane words (see the layout note at the top).
 __global__ void sp24_meta_kernel(const uint32_t* __restrict__ nib_tmp, int64_t total_rows, uint32_t* sp_meta) {
-  const int64_t n = total_rows * 4;  // (row-of-lane, j)
+  const int64_t n = total_rows * 4;  // (row-of-lane, j); output words 8 per row
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t lane_row = i >> 2;
     const int j = (int)(i & 3);
@@ -160,7 +162,7 @@ __global__ void sp24_meta_kernel(const uint32_t* __restrict__ nib_tmp, int64_t t
         w |= nibble << (4 * c + 16 * m1);
       }
     }
-    sp_meta[i] = w;
+    sp_meta[lane_row * 8 + 4 * (j >> 1) + (j & 1)] = w;
   }
 }
 
@@ -255,6 +257,7 @@ extern "C" int rb_sparse24_emit(const rb_vbr_device* v, const int64_t* sp_tile_r
           a, (const __half*)v->tiles, (__half*)sp_tiles, nib_tmp, nullptr, res_ptr, res_col, res_val, total_threads,
           thread_base);
     RB_CUDA_TRY(cudaGetLastError());
+    RB_CUDA_TRY(cudaMemsetAsync(sp_meta, 0, 32 * (size_t)total_sp_rows, stream));
     sp24_meta_kernel<<<grid_of(total_sp_rows * 4), 256, 0, stream>>>(nib_tmp, total_sp_rows, sp_meta);
     RB_CUDA_TRY(cudaGetLastError());
   }

@@ -339,19 +339,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 // ------------------------------------------------------------------------------------------
 // tall block rows on the 2:4 sparse tensor cores (tcgen05.mma.sp, cta_group::2, M=256 N=256 K=32
 // logical per MMA).  A stage = 128 logical K of the block row's padded block sequence: this CTA's
-// 128 compressed A rows (64 values, one SW128 TMA box of the sparse24.cu layout) + the 128 x 128
-// B panel half (four 64x64 boxes: K sub-ranges of 64 each inside one block) + 4 TMEM metadata
-// columns written by four metadata warps with tcgen05.st.  Single 256-column accumulator (TMEM
-// also holds the metadata ring), epilogue as the dense kernel.  The groups' extra nonzeros (more
-// than 2 of 4) are added by the residual pass after this kernel.
+// 128 compressed A rows (64 values, one SW128 TMA box of the sparse24.cu layout), the 128 x 128 B
+// panel half (four 64x64 boxes: K sub-ranges of 64 each inside one block) and this CTA's metadata
+// (two 2 KB planes: 128 lanes x 16 B).  The MMA thread moves the metadata to TMEM with two
+// tcgen05.cp 128x128b (ordered before its MMAs in the tensor pipe) and points MMA j at the
+// 4-column-aligned plane j/2 with idesc sparse_id2 = j%2 (tools/sp_probe).  Single 256-column
+// accumulator (TMEM also holds the metadata ring); epilogue as the dense kernel.  Groups' extra
+// nonzeros (more than 2 of 4) are added by the residual pass after this kernel.
 constexpr int SP_STAGES = 4;
-constexpr int SP_THREADS = 320;  // warp 0 TMA, 1 MMA, 2-5 epilogue, 6-9 metadata
+constexpr int SP_THREADS = 192;  // warp 0 TMA, 1 MMA, 2-5 epilogue
 constexpr uint32_t SP_A_BYTES = 128 * 128;
 constexpr uint32_t SP_B_BYTES = 4 * BOX_BYTES;
-constexpr uint32_t SP_STAGE_BYTES = SP_A_BYTES + SP_B_BYTES;  // 48 KB
-constexpr uint32_t SP_META_BYTES = 128 * 16;  // this CTA's 128 lanes x 4 metadata words per stage
-constexpr uint32_t SMEM_SP = SP_STAGES * (SP_STAGE_BYTES + SP_META_BYTES) + 1024 + 512;
-constexpr uint32_t SP_META_COL = 256;  // TMEM column of the metadata ring: + 16 * stage + 4 * j
+constexpr uint32_t SP_E_PLANE = 128 * 16;
+constexpr uint32_t SP_STAGE_BYTES = SP_A_BYTES + SP_B_BYTES + 2 * SP_E_PLANE;  // 52 KB
+constexpr uint32_t SMEM_SP = SP_STAGES * SP_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t SP_META_COL = 256;  // TMEM metadata ring: + 8 * stage + 4 * plane
 
 __device__ __forceinline__ void umma_sp_2sm(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t e_tmem,
                                             uint32_t acc) {
@@ -361,22 +363,24 @@ __device__ __forceinline__ void umma_sp_2sm(uint32_t d, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(e_tmem)
       : "memory");
 }
-__device__ __forceinline__ void tmem_st_32x32b_x1(uint32_t taddr, uint32_t v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+// 128 lanes x 128 bits from shared memory (128 rows of 16 B, no swizzle) into 4 TMEM columns of both CTAs
+__device__ __forceinline__ void tmem_cp_128x128b_2sm(uint32_t taddr, uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO 16 B (single core matrix along K)
+  d |= (uint64_t)(128 >> 4) << 32;   // SBO: 8-row core matrices 128 B apart
+  d |= (uint64_t)1 << 46;            // version
+  asm volatile("tcgen05.cp.cta_group::2.128x128b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
 }
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
     spmm_tall2_sp_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmE, SpmmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* smeta = smem + SP_STAGES * SP_STAGE_BYTES;  // [stage][128 lanes][16 B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smeta + SP_STAGES * SP_META_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SP_STAGES * SP_STAGE_BYTES);
   uint64_t* empty = full + SP_STAGES;
-  uint64_t* mfull = empty + SP_STAGES;
-  uint64_t* mload = mfull + SP_STAGES;  // per-CTA: this CTA's metadata rows landed (local TMA)
-  uint64_t* tfull = mload + SP_STAGES;
+  uint64_t* tfull = empty + SP_STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
@@ -389,8 +393,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
     for (int s = 0; s < SP_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&mfull[s], 8);  // 4 metadata warps x 2 CTAs
-      mbar_init(&mload[s], 1);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs
@@ -405,11 +407,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: compressed A rows + B panel half, both CTAs
+      // ---------------- TMA producer: compressed A rows + metadata planes + B panel half, both CTAs
       tma_prefetch_desc(&tmS);
       tma_prefetch_desc(&tmB);
       tma_prefetch_desc(&tmE);
-      const uint64_t pol_a = policy_evict_normal();
+      const uint64_t pol_a = policy_evict_normal();  // compressed A is re-read by the next N chunk
       const uint64_t pol_b = policy_evict_last();
       PipeState ps;
       for (int i = pair; i < a.n_items; i += n_pairs) {
@@ -426,10 +428,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[ps.s], 2 * SP_STAGE_BYTES);
           uint8_t* sA = smem + ps.s * SP_STAGE_BYTES;
           uint8_t* sB = sA + SP_A_BYTES;
-          tma_load_2d_2sm(sA, &tmS, &full[ps.s], 0, (int32_t)(row0 + (int64_t)s * hs), pol_a);
-          // this CTA's metadata rows, local barrier (read by this CTA's metadata warps)
-          mbar_arrive_expect_tx(&mload[ps.s], SP_META_BYTES);
-          tma_load_2d(smeta + ps.s * SP_META_BYTES, &tmE, &mload[ps.s], 0, (int32_t)(row0 + (int64_t)s * hs));
+          uint8_t* sE = sB + SP_B_BYTES;
+          const int32_t r = (int32_t)(row0 + (int64_t)s * hs);
+          tma_load_2d_2sm(sA, &tmS, &full[ps.s], 0, r, pol_a);
+          tma_load_2d_2sm(sE, &tmE, &full[ps.s], 0, r, pol_a);
+          tma_load_2d_2sm(sE + SP_E_PLANE, &tmE, &full[ps.s], 4, r, pol_a);
           const int nb0 = n0 + (int)rank * 128;
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
@@ -449,7 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      // ---------------- sparse MMA issuer
+      // ---------------- metadata copies + sparse MMAs (one thread, in tensor-pipe order)
       const uint32_t idesc = idesc_f16(256, TALL_BN, a.ab_fmt, /*a_mn=*/0, /*b_mn=*/1) | (1u << 2);
       PipeState ps;
       uint32_t aph = 0;
@@ -460,42 +463,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
         tc_fence_after();
         for (int s = k0; s < k1; ++s) {
           mbar_wait(&full[ps.s], ps.ph);
-          mbar_wait(&mfull[ps.s], ps.ph);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + ps.s * SP_STAGE_BYTES);
           const uint32_t b_base = a_base + SP_A_BYTES;
+          const uint32_t e_base = b_base + SP_B_BYTES;
+          const uint32_t e_tmem = tmem + SP_META_COL + 8 * ps.s;
+          tmem_cp_128x128b_2sm(e_tmem, e_base);
+          tmem_cp_128x128b_2sm(e_tmem + 4, e_base + SP_E_PLANE);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint64_t ad = sdesc_sw128(a_base + j * 32, 16, 1024);  // 16 compressed values
             const uint64_t bd = sdesc_sw128(b_base + (j >> 1) * 2 * BOX_BYTES + (j & 1) * 4096, BOX_BYTES, 1024);
-            umma_sp_2sm(tmem, ad, bd, idesc, tmem + SP_META_COL + 16 * ps.s + 4 * j, (s != k0) || j != 0);
+            umma_sp_2sm(tmem, ad, bd, idesc | (uint32_t)(j & 1), e_tmem + 4 * (j >> 1), (s != k0) || j != 0);
           }
           umma_commit_2sm_mc(&empty[ps.s], 0x3);
           ps.advance(SP_STAGES);
         }
         umma_commit_2sm_mc(tfull, 0x3);
         aph ^= 1;
-      }
-    }
-  } else if (warp >= 6) {
-    // ---------------- metadata writers: TMEM lane quadrant of this warp, 4 words per stage
-    const int quad = warp & 3;
-    PipeState ps;
-    for (int i = pair; i < a.n_items; i += n_pairs) {
-      const int4 it = a.items[2 * i], iu = a.items[2 * i + 1];
-      for (int s = it.w; s < iu.x; ++s) {
-        mbar_wait(&mload[ps.s], ps.ph);  // implies the slot's previous MMAs are done (producer waited empty)
-        const uint4 w = *reinterpret_cast<const uint4*>(smeta + ps.s * SP_META_BYTES + (quad * 32 + lane) * 16);
-        const uint32_t col = tmem + ((uint32_t)(quad * 32) << 16) + SP_META_COL + 16 * ps.s;
-        tmem_st_32x32b_x1(col + 0, w.x);
-        tmem_st_32x32b_x1(col + 4, w.y);
-        tmem_st_32x32b_x1(col + 8, w.z);
-        tmem_st_32x32b_x1(col + 12, w.w);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&mfull[ps.s]);
-        ps.advance(SP_STAGES);
       }
     }
   } else {
@@ -1277,7 +1262,7 @@ extern "C" int rb_spmm_plan_attach_sparse24(rb_spmm_plan* p, const rb_sparse24_d
         p->b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     int rc = make_tmap_2d(&p->tmSP, sp->sp_tiles, dt, 64, (uint64_t)sp->total_sp_rows, 128, 64, 128);
     if (!rc)
-      rc = make_tmap_2d(&p->tmSPE, sp->sp_meta, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, (uint64_t)sp->total_sp_rows, 16, 4,
+      rc = make_tmap_2d(&p->tmSPE, sp->sp_meta, CU_TENSOR_MAP_DATA_TYPE_UINT32, 8, (uint64_t)sp->total_sp_rows, 32, 4,
                         128, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
   }

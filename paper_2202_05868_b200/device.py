@@ -279,7 +279,7 @@ class DeviceVbr:
             "tall_g": torch.from_numpy(tall_g if len(tall_g) else np.zeros(1, np.int32)).to(dev),
             "tbase": torch.from_numpy(tbase).to(dev),
             "tiles": torch.zeros((max(total.value, 1), 64), dtype=L.TORCH_DTYPE[td], device=dev),
-            "meta": torch.zeros(max(total.value, 1) * 4, dtype=torch.int32, device=dev),
+            "meta": torch.zeros(max(total.value, 1) * 8, dtype=torch.int32, device=dev),
             "res_ptr": torch.zeros(self.n_rows + 1, dtype=torch.int64, device=dev),
         }
         wsb = ctypes.c_size_t(0)
