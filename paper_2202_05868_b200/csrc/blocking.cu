@@ -760,10 +760,14 @@ struct SGreedyArgs {
   int32_t* scratch;  // per block: overflow of the pattern list arrays, 3 x (n_seg+1)
   unsigned long long* stats;  // [8] counters (block 0): batches, batch seeds, singletons, rounds, accepts,
                               //     cycles in BATCH, cycles in GROUP, batch-skips
+  int64_t batch_max_enum;
 };
 
 constexpr int kPlistSmem = 4096;
-constexpr int64_t kBatchMaxEnum = 4 * kSparseThreads;  // speculative CTA enumerates at most this many entries  // pattern-list entries held in shared memory (the rest in scratch)
+// A speculative CTA enumerates at most batch_max_enum candidate entries (SGreedyArgs); larger
+// candidate sets go to the all-CTA GROUP round.  24 x 512 measured best on config 3 (R-MAT 2^20):
+// tau 0.7 3.60 -> 2.08 s, 0.3 6.51 -> 5.95 s vs 4 x 512 (RB_1SA_BATCH_ENUM overrides).
+constexpr int64_t kBatchMaxEnumDefault = 24 * kSparseThreads;
 
 // The pattern's segment list and its prefix-enumeration arrays (start, exclusive-scan of lengths).
 struct PList {
@@ -1044,7 +1048,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
         const int64_t total = prepare_round(a, pl, bs, psize, my + 1, &mode, &emp_lo);
         // a seed with a large candidate set is not tested speculatively by one CTA: reporting "unknown"
         // (treated as a hit) ends the singleton run here and the GROUP protocol (all CTAs) takes it
-        if (total > kBatchMaxEnum && threadIdx.x == 0) bs.flag = 2;
+        if (total > a.batch_max_enum && threadIdx.x == 0) bs.flag = 2;
         __syncthreads();
         for (int64_t e0 = 0; e0 < total && !bs.flag; e0 += blockDim.x) {
           const int64_t e = e0 + threadIdx.x;
@@ -1387,6 +1391,8 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     ga.ctrl = ws.ctrl;
     ga.scratch = ws.scratch;
     ga.stats = ws.stats;
+    ga.batch_max_enum = kBatchMaxEnumDefault;
+    if (const char* e = std::getenv("RB_1SA_BATCH_ENUM")) ga.batch_max_enum = std::max<int64_t>(0, std::atoll(e));
     RB_CUDA_TRY(cudaMemsetAsync(ws.stats, 0, 8 * 8, stream));
     const size_t shm = sizeof(uint64_t) * W + sizeof(int32_t) * 3 * kPlistSmem;
     if (shm > 200 * 1024) return fail(RB_EUNSUPPORTED, "too many segments for the pattern bitset in shared memory");
