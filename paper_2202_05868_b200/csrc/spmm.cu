@@ -1034,6 +1034,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   std::vector<int32_t> zero_rows;  // permuted positions of the rows of empty block rows
   int64_t sk_slots = 0, sk_units = 0;
   std::vector<int32_t> short_rows;
+  std::vector<int2> skinny_rows;  // (g, nb), turned into items once the class totals are known
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
@@ -1044,7 +1045,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       continue;
     }
     if (h <= skinny_h) {
-      skinny_items_for_row((int32_t)g, h, bp[g], nb, N, sk_cols, skinny[skinny_class(h)], sk_slots, sk_units);
+      skinny_rows.push_back(make_int2((int)g, nb));
       exec_flops += 2.0 * nb * h * (double)vbr->dp * N;
       vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
       core_vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
@@ -1067,6 +1068,29 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
         exec_flops += 2.0 * nb * dpc * KCH * PAIR_BM * (double)((N + TALL_BN - 1) / TALL_BN * TALL_BN);
         vbr_flops += 2.0 * nb * std::min(PAIR_BM, h - m * PAIR_BM) * (double)vbr->dp * N;
       }
+    }
+  }
+  {
+    // Part size per height class: hub rows are always cut at SKINNY_PART_BLOCKS; a class with little
+    // work (config 1's few 4..8-row block rows) is cut finer so that ~8 units per SM exist — a part
+    // is a serial chain of staged batches, and one group working through a 30-block row alone is
+    // the whole step's latency.
+    int64_t cls_blocks[SKINNY_CLASSES] = {0, 0, 0, 0};
+    for (const int2& r : skinny_rows) cls_blocks[skinny_class(rp[r.x + 1] - rp[r.x])] += r.y;
+    int dev_ = 0, sms_ = kNumSMs;
+    RB_CUDA_TRY(cudaGetDevice(&dev_));
+    RB_CUDA_TRY(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_));
+    const int64_t target = 8LL * sms_;
+    int part[SKINNY_CLASSES];
+    for (int c = 0; c < SKINNY_CLASSES; ++c) {
+      const int nb_batch = std::max(2, 32 / skinny_class_h(c));  // blocks per staged batch (LPR / H)
+      const int64_t want = (cls_blocks[c] + target - 1) / std::max<int64_t>(target, 1);
+      part[c] = (int)std::min<int64_t>(SKINNY_PART_BLOCKS, std::max<int64_t>(2 * nb_batch, want));
+    }
+    for (const int2& r : skinny_rows) {
+      const int h = rp[r.x + 1] - rp[r.x];
+      const int c = skinny_class(h);
+      skinny_items_for_row(r.x, h, bp[r.x], r.y, N, sk_cols, skinny[c], sk_slots, sk_units, part[c]);
     }
   }
   if (short_g_major) {

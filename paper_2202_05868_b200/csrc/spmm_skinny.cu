@@ -610,9 +610,10 @@ int skinny_cols(int32_t b_dtype, int64_t N) {
 }
 
 void skinny_items_for_row(int32_t g, int h, int32_t blk_begin, int nb, int64_t N, int cols,
-                          std::vector<SkinnyItem>& out, int64_t& n_slots, int64_t& ws_units) {
+                          std::vector<SkinnyItem>& out, int64_t& n_slots, int64_t& ws_units, int part_blocks) {
   const int H = skinny_class_h(skinny_class(h));
-  const int nparts = nb > SKINNY_PART_BLOCKS ? (nb + SKINNY_PART_BLOCKS - 1) / SKINNY_PART_BLOCKS : 1;
+  const int pb = std::max(1, part_blocks);
+  const int nparts = nb > pb ? (nb + pb - 1) / pb : 1;
   for (int64_t n0 = 0; n0 < N; n0 += cols) {
     if (nparts == 1) {
       out.push_back(SkinnyItem{g, (int32_t)n0, blk_begin, blk_begin + nb, 0, 1, -1, 0});

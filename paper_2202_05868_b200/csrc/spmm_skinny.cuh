@@ -60,7 +60,8 @@ int skinny_cols(int32_t b_dtype, int64_t N);
 // slab; rows with more than SKINNY_PART_BLOCKS blocks are split (slot / workspace bookkeeping in
 // n_slots and ws_units, in 128-float units).
 void skinny_items_for_row(int32_t g, int h, int32_t blk_begin, int nb, int64_t N, int cols,
-                          std::vector<SkinnyItem>& out, int64_t& n_slots, int64_t& ws_units);
+                          std::vector<SkinnyItem>& out, int64_t& n_slots, int64_t& ws_units,
+                          int part_blocks = SKINNY_PART_BLOCKS);
 
 // Launches the class-`cls` kernel over a.items[0 .. a.n_items) (persistent grid; `sched` = two
 // zero-initialised device counters owned by the plan, reset by the kernel itself on exit).

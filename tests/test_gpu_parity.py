@@ -312,8 +312,9 @@ def _grouped_matrix(rng, heights, n_cols, delta, density):
 def test_spmm_skinny_block_rows(precision, N, ld, monkeypatch):
     """Block rows with h <= 8 run on the CUDA-core skinny kernel (every height class, lane groups of
     16 and 32, unaligned fp32 B rows, ragged N, empty block rows).  C within tolerance of the
-    float64 product of the same rounded inputs; on the fp32 path bit-identical to the dense-tile
-    SIMT kernel (RB_SKINNY_H=0), since the skipped terms are exact zeros."""
+    float64 product of the same rounded inputs; on the fp32 path within 1e-6 of the dense-tile
+    SIMT kernel (RB_SKINNY_H=0): skipped terms are exact zeros, but block rows may be cut into parts
+    summed separately (small classes are split for parallelism), which reorders the fp32 sums."""
     from paper_2202_05868_b200 import _lib as L
     from paper_2202_05868_b200.device import DeviceCsr, DeviceVbr
 
@@ -341,7 +342,8 @@ def test_spmm_skinny_block_rows(precision, N, ld, monkeypatch):
     tol = 1e-5 if precision == "fp32" else 1e-4
     assert_close(Cs["8"].cpu().numpy().astype(np.float64), ref, bound, tol, f"skinny {precision}")
     if precision == "fp32":
-        assert torch.equal(Cs["8"], Cs["0"])
+        assert_close(Cs["8"].cpu().numpy().astype(np.float64), Cs["0"].cpu().numpy().astype(np.float64), bound,
+                     1e-6, "skinny vs simt")
     else:
         assert_close(Cs["0"].cpu().numpy().astype(np.float64), ref, bound, tol, f"tensor {precision}")
 
