@@ -30,6 +30,7 @@ namespace {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline int64_t words_of(int64_t n_seg) { return n_seg > 0 ? (n_seg + 63) / 64 : 1; }
+constexpr int kMaxTesters = 4096;  // speculative seeds per batch of the dense greedy (one per warp)
 inline unsigned grid_for(int64_t work, int per_block) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, 148 * 16));
 }
@@ -91,7 +92,7 @@ Ws carve(void* base, int64_t n, int64_t W, int64_t n_seg) {
   w.group_of_item = (int32_t*)take(sizeof(int32_t) * n1);
   w.seed_item = (int32_t*)take(sizeof(int32_t) * n1);
   w.ok = (uint8_t*)take(n1);
-  w.ctrl = (int32_t*)take(sizeof(int32_t) * 16);
+  w.ctrl = (int32_t*)take(sizeof(int32_t) * (16 + 2 * kMaxTesters));
   w.keys_a = (unsigned long long*)take(sizeof(uint64_t) * n1);
   w.keys_b = (unsigned long long*)take(sizeof(uint64_t) * n1);
   w.vals_a = (int32_t*)take(sizeof(int32_t) * n1);
@@ -224,7 +225,9 @@ struct GreedyArgs {
   int32_t* group_of_item;  // [m], -1 = unassigned
   uint8_t* ok;             // [m] verdict of the latest evaluation
   int32_t* seed_item;      // [H]
-  int32_t* ctrl;           // [0..2] first growing hit, [3..5] first rejection, [6] H, [8] count, [9] gen
+  int32_t* ctrl;           // [0..2] first growing hit, [3..5] first rejection, [6] H, [8] count, [9] gen,
+                           // [10..12] ok counts, [16..16+2*kMaxTesters) speculative flags (two batches)
+  int32_t batching;        // speculative singleton batching enabled
 };
 
 // Merge predicate (blocking.py:239-248 == merge_condition 184-203), IEEE double, no contraction.
@@ -262,14 +265,25 @@ __device__ __forceinline__ void grid_barrier(int32_t* count, int32_t* gen) {
   __syncthreads();
 }
 
+// The greedy scan (blocking.py:209-266) with speculative singleton batching (exact):
+//  GROUP round: all CTAs evaluate every unassigned item >= pos against the pattern; the first
+//         growing hit grows the pattern, a complete group seeds the next one at its first rejection.
+//  BATCH: after a singleton group (one round, nothing accepted) every warp takes one of the next K
+//         unassigned items as a speculative seed and tests whether ANY later unassigned item passes
+//         the merge test against it.  Seeds before the first one with a hit are singleton groups in
+//         the sequential scan too (a singleton assigns only itself, never a candidate of a later
+//         seed), so they are committed in order at once; the first seed with a hit starts a GROUP.
+//         A batch whose first seed has a hit backs off (2^k later groups skip batching).
 template <bool kWarpPerItem>
 __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
   extern __shared__ unsigned long long sP[];  // current pattern, W words
-  __shared__ int32_t s_js, s_rj;
+  __shared__ int32_t s_js, s_rj, s_ok;
   __shared__ int32_t s_pos, s_g, s_first_rej, s_acc_lo, s_acc_hi, s_acc_g, s_finishing;
+  __shared__ int32_t s_mode, s_grounds, s_cursor, s_batch, s_backoff, s_skip, s_len, s_f;
   __shared__ long long s_psize;
   __shared__ double s_cap;
   __shared__ int32_t s_inter;
+  __shared__ int32_t s_list[kMaxTesters];
 
   const int32_t m = a.m, W = a.W;
   const double tau = a.tau;
@@ -281,6 +295,11 @@ __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
     s_acc_lo = s_acc_hi = 0;
     s_acc_g = 0;
     s_finishing = 0;
+    s_mode = 0;
+    s_grounds = 0;
+    s_batch = 0;
+    s_backoff = 0;
+    s_skip = 0;
     s_psize = a.sizes[0];
     s_cap = __ddiv_rn((double)a.sizes[0], cap_den);
     if (blockIdx.x == 0) {
@@ -291,19 +310,121 @@ __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
   for (int w = threadIdx.x; w < W; w += blockDim.x) sP[w] = a.bits[w];
   __syncthreads();
 
-  const int lane = threadIdx.x & 31;
-  for (int r = 0;; ++r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int32_t K = min((int32_t)(gridDim.x * nwarps), (int32_t)kMaxTesters);
+  for (int r = 0;;) {
+    if (s_mode == 1) {
+      // ============================ BATCH: speculative singleton seeds, one per warp
+      if (warp == 0) {
+        int32_t cnt = 0;
+        for (int32_t j0 = s_cursor; j0 < m && cnt < K; j0 += 32) {
+          const int32_t j = j0 + lane;
+          const bool un = j < m && __ldcg(a.group_of_item + j) < 0;
+          const unsigned b = __ballot_sync(0xffffffffu, un);
+          const int32_t rk = __popc(b & ((1u << lane) - 1u));
+          if (un && cnt + rk < K) s_list[cnt + rk] = j;
+          cnt += __popc(b);
+        }
+        if (lane == 0) s_len = min(cnt, K);
+      }
+      __syncthreads();
+      const int32_t len = s_len, batch = s_batch;
+      if (len == 0) break;  // every item is assigned
+      int32_t* flags = a.ctrl + 16 + (batch & 1) * kMaxTesters;
+      const int32_t t = (int32_t)blockIdx.x * nwarps + warp;
+      if (t < len) {
+        const int32_t seed = s_list[t];
+        const unsigned long long* bs = a.bits + (int64_t)seed * W;
+        const int64_t ps = a.sizes[seed];
+        const double cap = __ddiv_rn((double)ps, cap_den);
+        bool hit = false;
+        for (int32_t j0 = seed + 1; j0 < m && !hit; j0 += 32) {
+          const int32_t j = j0 + lane;
+          bool v = false;
+          if (j < m && __ldcg(a.group_of_item + j) < 0) {
+            const unsigned long long* bj = a.bits + (int64_t)j * W;
+            int64_t inter = 0;
+            for (int w = 0; w < W; ++w) inter += __popcll(__ldg(bj + w) & __ldg(bs + w));
+            v = accept_dev(inter, ps, a.sizes[j], tau, a.cosine, a.bounded, cap);
+          }
+          hit = __any_sync(0xffffffffu, v);
+        }
+        if (lane == 0) flags[t] = hit ? 1 : 0;
+      }
+      grid_barrier(a.ctrl + 8, a.ctrl + 9);
+      if (warp == 0) {
+        int32_t f = len;
+        for (int32_t k0 = 0; k0 < len; k0 += 32) {
+          const int32_t k = k0 + lane;
+          const bool hit = k < len && *((volatile const int32_t*)(flags + k)) != 0;
+          const unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (b) {
+            f = k0 + __ffs(b) - 1;
+            break;
+          }
+        }
+        if (lane == 0) s_f = f;
+      }
+      __syncthreads();
+      const int32_t f = s_f, g0 = s_g;
+      if (blockIdx.x == 0)  // singletons before the first hit, in order
+        for (int32_t k = threadIdx.x; k < f; k += blockDim.x) {
+          a.group_of_item[s_list[k]] = g0 + 1 + k;
+          a.seed_item[g0 + 1 + k] = s_list[k];
+        }
+      if (f == len) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          s_g = g0 + len;
+          s_cursor = s_list[len - 1] + 1;
+          s_batch = batch + 1;
+          s_backoff = 0;
+        }
+        __syncthreads();
+        continue;
+      }
+      const int32_t seed = s_list[f], gid = g0 + 1 + f;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+          a.group_of_item[seed] = gid;
+          a.seed_item[gid] = seed;
+        }
+        s_g = gid;
+        s_pos = seed + 1;
+        s_first_rej = INT_MAX;
+        s_acc_lo = s_acc_hi = 0;
+        s_psize = a.sizes[seed];
+        s_cap = __ddiv_rn((double)a.sizes[seed], cap_den);
+        s_grounds = 0;
+        s_batch = batch + 1;
+        if (f == 0) {  // wasted batch: back off
+          s_backoff = min(s_backoff + 1, 12);
+          s_skip = 1 << s_backoff;
+        } else {
+          s_backoff = 0;
+        }
+        s_mode = 0;
+      }
+      for (int w = threadIdx.x; w < W; w += blockDim.x) sP[w] = a.bits[(int64_t)seed * W + w];
+      __syncthreads();
+      continue;
+    }
+
+    // ============================ GROUP round
     const int slot = r % 3;
+    ++r;
     if (threadIdx.x == 0) {
       s_js = INT_MAX;
       s_rj = INT_MAX;
+      s_ok = 0;
     }
     __syncthreads();
     const int32_t pos = s_pos, acc_lo = s_acc_lo, acc_hi = s_acc_hi, acc_g = s_acc_g, g = s_g;
     const long long psize = s_psize;
     const double cap = s_cap;
     const int32_t lo = acc_lo < acc_hi ? min(acc_lo, pos) : pos;
-    int32_t my_js = INT_MAX, my_rj = INT_MAX;
+    int32_t my_js = INT_MAX, my_rj = INT_MAX, my_ok = 0;
     if (kWarpPerItem) {
       const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
       const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -323,6 +444,7 @@ __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
           const bool v = accept_dev(inter, psize, sz, tau, a.cosine, a.bounded, cap);
           if (lane == 0) {
             a.ok[j] = v;
+            my_ok += v;
             if (v && a.update && inter < sz) my_js = min(my_js, (int32_t)j);
             if (!v) my_rj = min(my_rj, (int32_t)j);
           }
@@ -344,6 +466,7 @@ __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
           const int64_t sz = a.sizes[j];
           const bool v = accept_dev(inter, psize, sz, tau, a.cosine, a.bounded, cap);
           a.ok[j] = v;
+          my_ok += v;
           if (v && a.update && inter < sz) my_js = min(my_js, (int32_t)j);
           if (!v) my_rj = min(my_rj, (int32_t)j);
         }
@@ -351,22 +474,27 @@ __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
     }
     my_js = __reduce_min_sync(0xffffffffu, my_js);
     my_rj = __reduce_min_sync(0xffffffffu, my_rj);
+    my_ok = __reduce_add_sync(0xffffffffu, my_ok);
     if (lane == 0) {
       if (my_js != INT_MAX) atomicMin(&s_js, my_js);
       if (my_rj != INT_MAX) atomicMin(&s_rj, my_rj);
+      if (my_ok) atomicAdd(&s_ok, my_ok);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       if (s_js != INT_MAX) atomicMin(a.ctrl + slot, s_js);
       if (s_rj != INT_MAX) atomicMin(a.ctrl + 3 + slot, s_rj);
+      if (s_ok) atomicAdd(a.ctrl + 10 + slot, s_ok);
     }
     grid_barrier(a.ctrl + 8, a.ctrl + 9);
     if (s_finishing) break;  // the final acceptance has been applied
     const int32_t js = *((volatile int32_t*)(a.ctrl + slot));
     const int32_t rj = *((volatile int32_t*)(a.ctrl + 3 + slot));
+    const int32_t okc = *((volatile int32_t*)(a.ctrl + 10 + slot));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.ctrl[(r + 2) % 3] = INT_MAX;
-      a.ctrl[3 + (r + 2) % 3] = INT_MAX;
+      a.ctrl[(slot + 2) % 3] = INT_MAX;
+      a.ctrl[3 + (slot + 2) % 3] = INT_MAX;
+      a.ctrl[10 + (slot + 2) % 3] = 0;
     }
     if (js < m) {
       // growth at js: accept ok items in [pos, js] (next phase), OR js's bits into the pattern
@@ -385,31 +513,40 @@ __global__ void __launch_bounds__(512) greedy_kernel(GreedyArgs a) {
         if (rj < js) s_first_rej = min(s_first_rej, rj);
         s_psize = psize + a.sizes[js] - s_inter;
         s_pos = js + 1;
+        s_grounds += 1;
       }
     } else {
       // the group is complete: accept ok items in [pos, m); the first rejected item seeds the next group
       const int32_t fr = min(s_first_rej, rj);
+      const bool singleton = s_grounds == 0 && okc == 0;
+      const bool to_batch = a.batching && singleton && fr < m && s_skip == 0;
       __syncthreads();
       if (threadIdx.x == 0) {
         s_acc_lo = pos;
         s_acc_hi = m;
         s_acc_g = g;
+        if (s_skip > 0) --s_skip;
         if (fr >= m) {
           s_finishing = 1;
           s_pos = m;
+        } else if (to_batch) {
+          s_acc_lo = s_acc_hi = 0;  // nothing was accepted
+          s_cursor = fr;
+          s_mode = 1;
         } else {
           s_g = g + 1;
           s_first_rej = INT_MAX;
           s_psize = a.sizes[fr];
           s_cap = __ddiv_rn((double)a.sizes[fr], cap_den);
           s_pos = fr + 1;
+          s_grounds = 0;
           if (blockIdx.x == 0) {
             a.group_of_item[fr] = g + 1;
             a.seed_item[g + 1] = fr;
           }
         }
       }
-      if (fr < m)
+      if (fr < m && !to_batch)
         for (int w = threadIdx.x; w < W; w += blockDim.x) sP[w] = a.bits[(int64_t)fr * W + w];
     }
     __syncthreads();
@@ -1538,6 +1675,7 @@ extern "C" int rb_block_1sa(int64_t n, int64_t n_cols, int64_t nnz, const int64_
     for (int i = 0; i < 16; ++i) ctrl0[i] = 0;
     for (int i = 0; i < 6; ++i) ctrl0[i] = INT_MAX;
     RB_CUDA_TRY(cudaMemcpyAsync(ws.ctrl, ctrl0, sizeof(ctrl0), cudaMemcpyHostToDevice, stream));
+    RB_CUDA_TRY(cudaMemsetAsync(ws.ctrl + 16, 0, sizeof(int32_t) * 2 * kMaxTesters, stream));
     GreedyArgs ga;
     ga.m = m;
     ga.W = (int32_t)W;
@@ -1551,6 +1689,8 @@ extern "C" int rb_block_1sa(int64_t n, int64_t n_cols, int64_t nnz, const int64_
     ga.ok = ws.ok;
     ga.seed_item = ws.seed_item;
     ga.ctrl = ws.ctrl;
+    ga.batching = 1;
+    if (const char* e = std::getenv("RB_1SA_BATCH")) ga.batching = std::atoi(e) != 0;
     const bool warp_item = W > 4;
     const size_t shm = sizeof(uint64_t) * W;
     if (shm > 200 * 1024) return fail(RB_EUNSUPPORTED, "too many segments for the dense-bitset scan");
