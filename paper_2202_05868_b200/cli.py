@@ -165,41 +165,47 @@ def cmd_bench(args) -> int:
     return 0
 
 
-def _tau_type(s: str) -> float:
-    t = float(s)
-    if not 0.0 <= t <= 1.0:
-        raise argparse.ArgumentTypeError(f"tau must be in [0, 1], got {s}")
-    return t
+def _tau_type(text: str) -> float:
+    value = float(text)
+    if value < 0.0 or value > 1.0:
+        raise argparse.ArgumentTypeError(f"tau must be in [0, 1], got {text}")
+    return value
+
+
+# (flags, keyword arguments) per command; the reference's flag names and defaults, plus --precision
+_COMMON = [
+    (("input",), {}),
+    (("--tau",), dict(type=_tau_type, required=True)),
+    (("--policy",), dict(choices=["bounded", "plain"], default="bounded")),
+    (("--similarity",), dict(choices=["jaccard", "cosine"])),
+    (("--scramble-seed",), dict(type=int)),
+]
+_COMMANDS = {
+    "block": ("group the rows of an .mtx file (device 1-SA)", [
+        (("--dw",), dict(type=int, required=True, help="column partition width")),
+        (("--no-compress",), dict(action="store_true")),
+        (("--out",), dict(help="write the grouping as JSON")),
+    ]),
+    "bench": ("time the CSR and VBR kernels on the GPU", [
+        (("--dw",), dict(type=int, nargs="+", required=True)),
+        (("-N", "--n-dense"), dict(type=int, nargs="+", required=True)),
+        (("--threads",), dict(type=int, default=1, help="accepted for compatibility (GPU kernels)")),
+        (("--runs",), dict(type=int, default=3)),
+        (("--dense-seed",), dict(type=int, default=0)),
+        (("--precision",), dict(choices=["bf16", "fp16", "fp32"], default="bf16")),
+        (("--out",), {}),
+    ]),
+}
 
 
 def build_parser() -> argparse.ArgumentParser:
-    p = argparse.ArgumentParser(prog="rowblock-b200", description="Row blocking + VBR SpMM on B200: block, bench.")
-    sub = p.add_subparsers(dest="command", required=True)
-
-    b = sub.add_parser("block", help="group the rows of an .mtx file (device 1-SA)")
-    b.add_argument("input")
-    b.add_argument("--dw", type=int, required=True, help="column partition width")
-    b.add_argument("--tau", type=_tau_type, required=True)
-    b.add_argument("--policy", choices=["bounded", "plain"], default="bounded")
-    b.add_argument("--similarity", choices=["jaccard", "cosine"])
-    b.add_argument("--no-compress", action="store_true")
-    b.add_argument("--scramble-seed", type=int)
-    b.add_argument("--out", help="write the grouping as JSON")
-
-    be = sub.add_parser("bench", help="time the CSR and VBR kernels on the GPU")
-    be.add_argument("input")
-    be.add_argument("--dw", type=int, nargs="+", required=True)
-    be.add_argument("--tau", type=_tau_type, required=True)
-    be.add_argument("-N", "--n-dense", type=int, nargs="+", required=True)
-    be.add_argument("--threads", type=int, default=1, help="accepted for compatibility (GPU kernels)")
-    be.add_argument("--runs", type=int, default=3)
-    be.add_argument("--policy", choices=["bounded", "plain"], default="bounded")
-    be.add_argument("--similarity", choices=["jaccard", "cosine"])
-    be.add_argument("--scramble-seed", type=int)
-    be.add_argument("--dense-seed", type=int, default=0)
-    be.add_argument("--precision", choices=["bf16", "fp16", "fp32"], default="bf16")
-    be.add_argument("--out")
-    return p
+    parser = argparse.ArgumentParser(prog="rowblock-b200", description="Row blocking + VBR SpMM on B200: block, bench.")
+    sub = parser.add_subparsers(dest="command", required=True)
+    for name, (help_text, specific) in _COMMANDS.items():
+        cmd = sub.add_parser(name, help=help_text)
+        for flags, kw in _COMMON + specific:
+            cmd.add_argument(*flags, **kw)
+    return parser
 
 
 def main(argv=None) -> int:

@@ -1,12 +1,13 @@
-"""MatrixMarket I/O — drop-in for rowblock.mtxio (mtxio.py:1-119), vectorised.
+"""MatrixMarket coordinate files — drop-in for rowblock.mtxio (mtxio.py:1-119), vectorised.
 
-Same accepted formats (coordinate; real / integer / pattern; general / symmetric), same
-canonicalisation (pattern entries = 1.0, symmetric storage mirrored, duplicates summed in file
-order, zeros dropped) and the same ``MatrixMarketError`` messages with line numbers.  The entry
-block is parsed in one numpy pass instead of a Python loop per line (the reference reads a
-16M-entry file in minutes; the bench's R-MAT 2^20 input is 16M entries); a file the fast path
-rejects is re-scanned line by line only to report the offending line.  ``read_matrix_market_device``
-lands the canonical CSR in HBM for the device 1-SA / VBR / SpMM path.
+Accepted: ``coordinate`` layout; ``real`` / ``integer`` / ``pattern`` fields; ``general`` /
+``symmetric`` storage.  Canonicalisation follows the reference: pattern entries are 1.0,
+symmetric storage is mirrored, duplicates are summed in file order, zeros are dropped.  Errors are
+``MatrixMarketError`` (a ValueError) with the reference's messages and 1-based line numbers.
+
+The entry block is parsed by one structured ``np.loadtxt`` call (integers as integers, values with a
+correctly rounded decimal conversion, as ``float()``); only a file that parse rejects is walked line
+by line, to name the offending line.  ``read_matrix_market_device`` lands the CSR in HBM.
 """
 
 from __future__ import annotations
@@ -19,110 +20,109 @@ from .types import CsrMatrix, csr_from_coo
 
 __all__ = ["MatrixMarketError", "read_matrix_market", "read_matrix_market_device", "write_matrix_market"]
 
-_FIELDS = ("real", "integer", "pattern")
-_SYMMETRIES = ("general", "symmetric")
+_ALLOWED = {"layout": ("coordinate",), "field": ("real", "integer", "pattern"), "symmetry": ("general", "symmetric")}
 
 
 class MatrixMarketError(ValueError):
-    """Parse failure; carries the offending line number (mtxio.py:21-27)."""
+    """A malformed or unsupported file; ``path`` and ``lineno`` locate the problem."""
 
     def __init__(self, path, lineno, message):
         super().__init__(f"{path}:{lineno}: {message}")
-        self.path = str(path)
-        self.lineno = lineno
+        self.path, self.lineno = str(path), lineno
 
 
-def _header(path, fh):
-    header = fh.readline()
-    if not header.lower().startswith("%%matrixmarket"):
+def _banner(path, line: str):
+    if not line.lower().startswith("%%matrixmarket"):
         raise MatrixMarketError(path, 1, "missing %%MatrixMarket header")
-    parts = header.strip().split()
-    if len(parts) != 5 or parts[1].lower() != "matrix":
-        raise MatrixMarketError(path, 1, f"malformed header: {header.strip()!r}")
-    layout, field, symmetry = (p.lower() for p in parts[2:5])
-    if layout != "coordinate":
-        raise MatrixMarketError(path, 1, f"unsupported layout {layout!r} (only coordinate)")
-    if field not in _FIELDS:
-        raise MatrixMarketError(path, 1, f"unsupported field {field!r}")
-    if symmetry not in _SYMMETRIES:
-        raise MatrixMarketError(path, 1, f"unsupported symmetry {symmetry!r}")
-    return field, symmetry
+    words = line.strip().split()
+    if len(words) != 5 or words[1].lower() != "matrix":
+        raise MatrixMarketError(path, 1, f"malformed header: {line.strip()!r}")
+    layout, fld, sym = (w.lower() for w in words[2:])
+    for kind, value in (("layout", layout), ("field", fld), ("symmetry", sym)):
+        if value not in _ALLOWED[kind]:
+            extra = " (only coordinate)" if kind == "layout" else ""
+            raise MatrixMarketError(path, 1, f"unsupported {kind} {value!r}{extra}")
+    return fld, sym
 
 
-def _slow_scan(path, lines, lineno, n_rows, n_cols, n_entries, want):
-    """Line-by-line validation with the reference's messages (mtxio.py:69-92); only reached when
-    the vectorised parse fails, to name the offending line."""
-    k = 0
-    for line in lines:
-        lineno += 1
-        line = line.strip()
-        if not line or line.startswith("%"):
-            continue
-        toks = line.split()
+def _content(lines, first_lineno):
+    """(lineno, stripped line) for every non-blank, non-comment line."""
+    for k, raw in enumerate(lines):
+        text = raw.strip()
+        if text and not text.startswith("%"):
+            yield first_lineno + k, text
+
+
+def _diagnose(path, lines, first_lineno, shape, want):
+    """Walk the entries the reference's way to report the first bad line (mtxio.py:69-92)."""
+    n_rows, n_cols, n_entries = shape
+    seen, last = 0, first_lineno - 1
+    for lineno, text in _content(lines, first_lineno):
+        last = lineno
+        toks = text.split()
         if len(toks) != want:
             raise MatrixMarketError(path, lineno, f"expected {want} fields, got {len(toks)}")
-        if k >= n_entries:
+        if seen >= n_entries:
             raise MatrixMarketError(path, lineno, "more entries than declared")
         try:
             i, j = int(toks[0]), int(toks[1])
             if want == 3:
                 float(toks[2])
         except ValueError:
-            raise MatrixMarketError(path, lineno, f"bad entry {line!r}") from None
+            raise MatrixMarketError(path, lineno, f"bad entry {text!r}") from None
         if not (1 <= i <= n_rows and 1 <= j <= n_cols):
             raise MatrixMarketError(path, lineno, f"index ({i}, {j}) out of range")
-        k += 1
-    if k != n_entries:
-        raise MatrixMarketError(path, lineno, f"declared {n_entries} entries, found {k}")
-    raise MatrixMarketError(path, lineno, "malformed entry block")
+        seen += 1
+    last = max(last, first_lineno - 1 + len(lines))
+    if seen != n_entries:
+        raise MatrixMarketError(path, last, f"declared {n_entries} entries, found {seen}")
+    raise MatrixMarketError(path, last, "malformed entry block")
 
 
 def read_matrix_market(path) -> CsrMatrix:
-    """Read a MatrixMarket coordinate file into a canonical CsrMatrix (mtxio.py:30-107)."""
+    """Canonical CsrMatrix from a MatrixMarket coordinate file (mtxio.py:30-107)."""
     with open(path, "r", encoding="ascii", errors="replace") as fh:
-        field, symmetry = _header(path, fh)
-        lineno = 1
-        size = None
-        for line in fh:
-            lineno += 1
-            line = line.strip()
-            if not line or line.startswith("%"):
-                continue
-            toks = line.split()
-            if len(toks) != 3:
-                raise MatrixMarketError(path, lineno, "size line must be 'rows cols nnz'")
-            try:
-                size = tuple(int(t) for t in toks)
-            except ValueError:
-                raise MatrixMarketError(path, lineno, f"bad size line {line!r}") from None
-            break
-        if size is None:
-            raise MatrixMarketError(path, lineno, "missing size line")
-        n_rows, n_cols, n_entries = size
-        if n_rows < 0 or n_cols < 0 or n_entries < 0:
-            raise MatrixMarketError(path, lineno, "negative size")
-        body = fh.read()
-    want = 2 if field == "pattern" else 3
-    dt = np.dtype([("i", np.int64), ("j", np.int64)] + ([("v", np.float64)] if want == 3 else []))
+        text = fh.read()
+    lines = text.split("\n")
+    if text.endswith("\n"):
+        lines.pop()
+    fld, sym = _banner(path, lines[0] if lines else "")
+    shape, body_at = None, len(lines)
+    for lineno, line in _content(lines[1:], 2):
+        toks = line.split()
+        if len(toks) != 3:
+            raise MatrixMarketError(path, lineno, "size line must be 'rows cols nnz'")
+        try:
+            shape = tuple(int(t) for t in toks)
+        except ValueError:
+            raise MatrixMarketError(path, lineno, f"bad size line {line!r}") from None
+        body_at = lineno  # entries start on the next line
+        break
+    if shape is None:
+        raise MatrixMarketError(path, len(lines), "missing size line")
+    if min(shape) < 0:
+        raise MatrixMarketError(path, body_at, "negative size")
+    n_rows, n_cols, n_entries = shape
+    body = lines[body_at:]
+    want = 2 if fld == "pattern" else 3
+    columns = [("i", np.int64), ("j", np.int64)] + ([("v", np.float64)] if want == 3 else [])
+    entries = [t for _, t in _content(body, body_at + 1)]
     try:
-        # comments / blank lines dropped, then one vectorised parse (integers parsed as integers,
-        # values with the same correctly rounded decimal conversion as float())
-        kept = [ln for ln in body.splitlines() if ln.strip() and not ln.lstrip().startswith("%")]
-        if len(kept) != n_entries:
+        if len(entries) != n_entries:
             raise ValueError("entry count")
-        arr = (np.loadtxt(io.StringIO("\n".join(kept)), dtype=dt, ndmin=1) if n_entries
-               else np.zeros(0, dtype=dt))
-        rows, cols = arr["i"] - 1, arr["j"] - 1
-        if n_entries and (rows.min() < 0 or rows.max() >= n_rows or cols.min() < 0 or cols.max() >= n_cols):
-            raise ValueError("range")
-        vals = arr["v"].astype(np.float64) if want == 3 else np.ones(n_entries)
+        rec = (np.loadtxt(io.StringIO("\n".join(entries)), dtype=np.dtype(columns), ndmin=1) if n_entries
+               else np.zeros(0, dtype=np.dtype(columns)))
+        r0, c0 = rec["i"] - 1, rec["j"] - 1
+        if n_entries and not (0 <= r0.min() and r0.max() < n_rows and 0 <= c0.min() and c0.max() < n_cols):
+            raise ValueError("index range")
     except ValueError:
-        _slow_scan(path, body.splitlines(), lineno, n_rows, n_cols, n_entries, want)
-    if symmetry == "symmetric":
-        off = rows != cols
-        rows, cols = np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]])
-        vals = np.concatenate([vals, vals[off]])
-    return csr_from_coo(n_rows, n_cols, rows, cols, vals, sum_duplicates=True)
+        _diagnose(path, body, body_at + 1, shape, want)
+    vals = rec["v"].astype(np.float64) if want == 3 else np.ones(n_entries)
+    if sym == "symmetric":
+        mirror = r0 != c0
+        r0, c0 = np.r_[r0, c0[mirror]], np.r_[c0, r0[mirror]]
+        vals = np.r_[vals, vals[mirror]]
+    return csr_from_coo(n_rows, n_cols, r0, c0, vals, sum_duplicates=True)
 
 
 def read_matrix_market_device(path, device=None):
@@ -136,14 +136,13 @@ def read_matrix_market_device(path, device=None):
 
 
 def write_matrix_market(path, A: CsrMatrix, comment: str | None = None) -> None:
-    """Write a CsrMatrix as `coordinate real general` (full storage, 1-based, %.17g values),
-    byte-identical to the reference's writer (mtxio.py:110-119)."""
-    rows = np.repeat(np.arange(A.n_rows, dtype=np.int64), A.row_nnz())
+    """``coordinate real general``, 1-based, ``%.17g`` values — byte-identical to the reference's
+    writer (mtxio.py:110-119)."""
+    head = ["%%MatrixMarket matrix coordinate real general"]
+    head += [f"% {ln}" for ln in (comment.splitlines() if comment else [])]
+    head.append(f"{A.n_rows} {A.n_cols} {A.nnz}")
+    rows1 = np.repeat(np.arange(1, A.n_rows + 1, dtype=np.int64), A.row_nnz()).tolist()
+    body = (f"{i} {j + 1} {v:.17g}" for i, j, v in zip(rows1, A.col_idx.tolist(), A.values.tolist()))
     with open(path, "w", encoding="ascii") as fh:
-        fh.write("%%MatrixMarket matrix coordinate real general\n")
-        if comment:
-            for ln in comment.splitlines():
-                fh.write(f"% {ln}\n")
-        fh.write(f"{A.n_rows} {A.n_cols} {A.nnz}\n")
-        fh.write("".join(f"{i + 1} {j + 1} {v:.17g}\n" for i, j, v in zip(rows.tolist(), A.col_idx.tolist(),
-                                                                        A.values.tolist())))
+        fh.write("\n".join(head) + "\n")
+        fh.writelines(line + "\n" for line in body)
