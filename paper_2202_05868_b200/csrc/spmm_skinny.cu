@@ -203,6 +203,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+constexpr int STAGED_WARPS = 4;  // 128-thread CTAs: 5 resident per SM (registers <= 102, 41 KB smem each)
+
 template <typename T, int LPR>
 struct SkinnySmem {
   static constexpr int KC = 64;                          // tile columns staged per block (dp <= 64)
@@ -211,7 +213,7 @@ struct SkinnySmem {
   static constexpr int STAGE = LPR * ROW;                // NB blocks x H rows = LPR staged rows
   static constexpr int CAP = 4 * LPR;                    // list entries per window
   static constexpr int GROUP_BYTES = 2 * STAGE + CAP * 8;
-  static constexpr int CTA_BYTES = 8 * (32 / LPR) * GROUP_BYTES;
+  static constexpr int CTA_BYTES = STAGED_WARPS * (32 / LPR) * GROUP_BYTES;
 };
 
 // Block rows of height h <= H (H = 1, 2, 4, 8), tiles at most 64 columns wide.  Per batch of
@@ -229,7 +231,7 @@ __device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyIte
   using S = SkinnySmem<T, LPR>;
   constexpr int VEC = 16 / sizeof(T);
   constexpr int NB = LPR / H;                 // blocks per batch
-  constexpr int DEPTH = H >= 4 ? 4 : 8;       // B gathers in flight per lane
+  constexpr int DEPTH = H >= 4 ? 4 : H == 1 ? 6 : 8;  // B gathers in flight per lane
   constexpr int ROWE = S::ROW / (int)sizeof(T);
   const int g = it.g;
   const int n = it.n0 + gl * VEC;
@@ -370,7 +372,7 @@ __device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyIte
 }
 
 template <typename T, int H, int LPR, bool ALIGNED>
-__global__ void __launch_bounds__(256, H == 1 ? 2 : 1) spmm_skinny_staged_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
+__global__ void __launch_bounds__(STAGED_WARPS * 32, H == 1 ? 5 : 2) spmm_skinny_staged_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
   using S = SkinnySmem<T, LPR>;
   constexpr int GPW = 32 / LPR;
   extern __shared__ uint4 smem_sk[];
@@ -530,11 +532,11 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_kernel(SkinnyArgs a, CsrArgs 
 }
 
 template <typename K>
-int persistent_grid(K kernel, int smem, int64_t n_items, int groups_per_cta, unsigned* grid) {
+int persistent_grid(K kernel, int smem, int64_t n_items, int groups_per_cta, unsigned* grid, int threads = 256) {
   int dev = 0, sms = kNumSMs, per_sm = 1;
   RB_CUDA_TRY(cudaGetDevice(&dev));
   RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  RB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem));
+  RB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
   const int64_t need = (n_items + groups_per_cta - 1) / groups_per_cta;
   *grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * std::max(1, per_sm)));
   return RB_OK;
@@ -555,9 +557,9 @@ int launch_t(const SkinnyArgs& a, int cols, unsigned long long* sched, cudaStrea
   } else {
     auto k = aligned ? spmm_skinny_staged_kernel<T, H, LPR, true> : spmm_skinny_staged_kernel<T, H, LPR, false>;
     RB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::CTA_BYTES));
-    int rc = persistent_grid(k, S::CTA_BYTES, a.n_items, per_cta, &grid);
+    int rc = persistent_grid(k, S::CTA_BYTES, a.n_items, STAGED_WARPS * (32 / LPR), &grid, STAGED_WARPS * 32);
     if (rc) return rc;
-    k<<<grid, 256, S::CTA_BYTES, stream>>>(a, cols, sched);
+    k<<<grid, STAGED_WARPS * 32, S::CTA_BYTES, stream>>>(a, cols, sched);
   }
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
