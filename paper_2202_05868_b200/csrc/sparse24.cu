@@ -82,7 +82,6 @@ __global__ void __launch_bounds__(256) sp24_rows_kernel(SpArgs a, const T* __res
     int64_t cnt = 0;
     for (int s = 0; s < S; ++s) {
       T vals[SP_STAGE_K];
-      uint32_t nz = 0;  // reused per 32-column quarter
       uint32_t words[4] = {0u, 0u, 0u, 0u};
       T comp[SP_PHYS];
 #pragma unroll 4
@@ -93,7 +92,6 @@ __global__ void __launch_bounds__(256) sp24_rows_kernel(SpArgs a, const T* __res
         if (live && t < nb) u = *reinterpret_cast<const uint4*>(tiles + (tbase + (int64_t)t * hp + r) * dp + c);
         memcpy(&vals[q], &u, 16);
       }
-      (void)nz;
       for (int ch = 0; ch < SP_STAGE_K / 4; ++ch) {
         int pos[4], np = 0;
 #pragma unroll
