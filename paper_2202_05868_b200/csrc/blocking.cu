@@ -918,24 +918,6 @@ struct PList {
   }
 };
 
-// warp-cooperative lower_bound (32-ary search): first index in [lo, hi) with arr[idx] >= key
-__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ arr, int64_t lo, int64_t hi,
-                                                    int32_t key, int lane) {
-  while (hi - lo > 32) {
-    const int64_t step = (hi - lo + 31) / 32;
-    const int64_t idx = lo + lane * step;
-    const bool less = idx < hi && __ldg(arr + idx) < key;
-    const int c = __popc(__ballot_sync(0xffffffffu, less));
-    if (c == 0) return lo;
-    const int64_t nlo = lo + (int64_t)(c - 1) * step + 1;
-    hi = min(hi, lo + (int64_t)c * step);
-    lo = nlo;
-  }
-  const int64_t idx = lo + lane;
-  const bool less = idx < hi && __ldg(arr + idx) < key;
-  return lo + __popc(__ballot_sync(0xffffffffu, less));
-}
-
 // block-wide exclusive scan of pl.scan(0..n), returns the total
 __device__ int32_t block_scan_plist(PList& pl, int32_t n, int32_t* smem_w /*[32]*/, int32_t* smem_carry) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;

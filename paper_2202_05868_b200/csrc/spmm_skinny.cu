@@ -433,7 +433,7 @@ __device__ __forceinline__ void skinny_item(const SkinnyArgs& a, const SkinnyIte
           nz |= v[r] != 0.f;
         }
         unsigned m = __ballot_sync(gmask, nz);
-        if (LPR < 32) m = (m >> (grp * LPR)) & ((1u << LPR) - 1u);
+        if constexpr (LPR < 32) m = (m >> (grp * LPR)) & ((1u << LPR) - 1u);
         const T* brow = B + (int64_t)(k0 + kc) * ldb;
         while (m) {
           int kk[4];
