@@ -21,6 +21,7 @@
 // spmm_simt_f32_kernel is the fp32 check path (tcgen05 has no fp32-exact MMA).
 #include <algorithm>
 #include <cstdlib>
+#include <functional>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <vector>
@@ -32,6 +33,7 @@
 namespace rb {
 
 constexpr int KCH = 64;                      // K elements per pipeline stage (one SW128 row)
+constexpr int kAuxStreams = 3;               // extra streams for concurrent launches of one SpMM
 constexpr int TC_THREADS = 192;
 constexpr uint32_t BOX_BYTES = 64 * 64 * 2;  // one [64 k x 64 n] B box (8 KB)
 constexpr int ACC_COLS = 256;                // TMEM columns per accumulator (x2 buffers)
@@ -908,6 +910,10 @@ struct rb_spmm_plan {
   rb::SkinnyItem* d_res_items = nullptr;
   int64_t n_res_items = 0;
   unsigned long long* d_res_sched = nullptr;
+  // fork/join streams of rb_spmm_execute (created on first use)
+  mutable bool aux_ready = false;
+  mutable cudaStream_t aux[rb::kAuxStreams] = {};
+  mutable cudaEvent_t ev[rb::kAuxStreams + 1] = {};
   float* d_skinny_ws = nullptr;     // partials of split skinny block rows
   int32_t* d_skinny_cnt = nullptr;
   unsigned long long* d_sched = nullptr;  // 2 work counters per skinny height class
@@ -1321,6 +1327,10 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_sp_cnt) cudaFree(p->d_sp_cnt);
   if (p->d_res_items) cudaFree(p->d_res_items);
   if (p->d_res_sched) cudaFree(p->d_res_sched);
+  if (p->aux_ready) {
+    for (int l = 0; l < kAuxStreams; ++l) cudaStreamDestroy(p->aux[l]);
+    for (int l = 0; l <= kAuxStreams; ++l) cudaEventDestroy(p->ev[l]);
+  }
   delete p;
   return RB_OK;
 }
@@ -1349,111 +1359,142 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.cnt = p->d_cnt;
   a.sp_meta = nullptr;
   a.sp_tile_row = nullptr;
-  if (p->n_zero > 0) {
-    const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
-    zero_rows_kernel<<<grid, 256, 0, stream>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc, (int32_t)p->N);
-    RB_CUDA_TRY(cudaGetLastError());
-  }
-  if (p->skinny_off[SKINNY_CLASSES] > 0) {
-    SkinnyArgs k{};
-    k.row_partition = p->v.row_partition;
-    k.row_perm = p->v.row_perm;
-    k.blk_ptr = p->v.blk_ptr;
-    k.blk_col = p->v.blk_col;
-    k.grp_tile_row = p->v.grp_tile_row;
-    k.col_bounds = p->v.col_bounds;
-    k.tiles = p->v.tiles;
-    k.dp = p->v.dp;
-    k.B = B;
-    k.ldb = ldb;
-    k.C = C;
-    k.ldc = ldc;
-    k.N = (int32_t)p->N;
-    k.ws = p->d_skinny_ws;
-    k.cnt = p->d_skinny_cnt;
-    for (int c = 0; c < SKINNY_CLASSES; ++c) {
-      k.items = p->d_skinny + p->skinny_off[c];
-      k.n_items = p->skinny_off[c + 1] - p->skinny_off[c];
-      int rc = launch_skinny(k, p->b_dtype, c, p->d_sched + 2 * c, stream);
-      if (rc) return rc;
-    }
-  }
-  if (p->b_dtype == RB_F32) {
-    if (p->n_simt > 0) {
-      a.items = p->d_items + 2 * p->n_tall + p->n_short;
-      a.n_items = (int32_t)p->n_simt;
-      a.dp_chunks = 1;
-      spmm_simt_f32_kernel<<<(unsigned)p->n_simt, SIMT_COLS, 0, stream>>>(
-          a, static_cast<const float*>(p->v.tiles), p->v.dp, static_cast<const float*>(B), ldb);
+  // Independent launches (disjoint C rows): zero rows, each skinny height class, the fp32 SIMT
+  // kernel, the tall and the short tensor-core kernels.  With more than one, they are forked over
+  // the caller's stream and up to three auxiliary streams and joined back (small latency-bound
+  // classes overlap the large kernels instead of queueing behind them).
+  std::vector<std::function<int(cudaStream_t)>> tasks;
+  if (p->n_zero > 0)
+    tasks.push_back([&](cudaStream_t st) {
+      const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
+      zero_rows_kernel<<<grid, 256, 0, st>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc, (int32_t)p->N);
       RB_CUDA_TRY(cudaGetLastError());
-    }
-    return RB_OK;
+      return RB_OK;
+    });
+  SkinnyArgs k{};
+  k.row_partition = p->v.row_partition;
+  k.row_perm = p->v.row_perm;
+  k.blk_ptr = p->v.blk_ptr;
+  k.blk_col = p->v.blk_col;
+  k.grp_tile_row = p->v.grp_tile_row;
+  k.col_bounds = p->v.col_bounds;
+  k.tiles = p->v.tiles;
+  k.dp = p->v.dp;
+  k.B = B;
+  k.ldb = ldb;
+  k.C = C;
+  k.ldc = ldc;
+  k.N = (int32_t)p->N;
+  k.ws = p->d_skinny_ws;
+  k.cnt = p->d_skinny_cnt;
+  for (int c = 0; c < SKINNY_CLASSES; ++c) {
+    if (p->skinny_off[c + 1] == p->skinny_off[c]) continue;
+    tasks.push_back([&, c](cudaStream_t st) {
+      SkinnyArgs kc = k;
+      kc.items = p->d_skinny + p->skinny_off[c];
+      kc.n_items = p->skinny_off[c + 1] - p->skinny_off[c];
+      return launch_skinny(kc, p->b_dtype, c, p->d_sched + 2 * c, st);
+    });
   }
-  static bool attr_done = false;
-  if (!attr_done) {
-    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
-    RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
-    attr_done = true;
-  }
+  if (p->b_dtype == RB_F32 && p->n_simt > 0)
+    tasks.push_back([&](cudaStream_t st) {
+      SpmmArgs s = a;
+      s.items = p->d_items + 2 * p->n_tall + p->n_short;
+      s.n_items = (int32_t)p->n_simt;
+      s.dp_chunks = 1;
+      spmm_simt_f32_kernel<<<(unsigned)p->n_simt, SIMT_COLS, 0, st>>>(
+          s, static_cast<const float*>(p->v.tiles), p->v.dp, static_cast<const float*>(B), ldb);
+      RB_CUDA_TRY(cudaGetLastError());
+      return RB_OK;
+    });
   CUtensorMap tmB;
   memset(&tmB, 0, sizeof(tmB));
-  if (p->v.n_blocks > 0) {
+  int sms = kNumSMs;
+  if (p->b_dtype != RB_F32 && (p->n_tall > 0 || p->n_short > 0)) {
+    static bool attr_done = false;
+    if (!attr_done) {
+      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
+      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
+      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
+      attr_done = true;
+    }
     const CUtensorMapDataType dt =
         p->b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     int rc = make_tmap_2d(&tmB, B, dt, (uint64_t)p->N, (uint64_t)p->v.n_cols, (uint64_t)ldb * 2, 64, 64);
     if (rc) return rc;
+    int dev = 0;
+    RB_CUDA_TRY(cudaGetDevice(&dev));
+    RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  int dev = 0, sms = kNumSMs;
-  RB_CUDA_TRY(cudaGetDevice(&dev));
-  RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (p->n_tall > 0 && p->use_sp) {
-    static bool sp_attr = false;
-    if (!sp_attr) {
-      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
-      sp_attr = true;
-    }
-    SpmmArgs s = a;
-    s.items = p->d_sp_units;
-    s.n_items = (int32_t)p->n_sp_units;
-    s.ws = p->d_sp_ws;
-    s.cnt = p->d_sp_cnt;
-    s.sp_meta = p->sp.sp_meta;
-    s.sp_tile_row = p->sp.sp_tile_row;
-    const int pairs = (int)std::min<int64_t>(sms / 2, p->n_sp_units);
-    if (pairs > 0) {
-      spmm_tall2_sp_kernel<<<(unsigned)(2 * pairs), SP_THREADS, SMEM_SP, stream>>>(p->tmSP, tmB, p->tmSPE, s);
+  if (p->b_dtype != RB_F32 && p->n_tall > 0)
+    tasks.push_back([&](cudaStream_t st) {
+      if (p->use_sp) {
+        SpmmArgs s = a;
+        s.items = p->d_sp_units;
+        s.n_items = (int32_t)p->n_sp_units;
+        s.ws = p->d_sp_ws;
+        s.cnt = p->d_sp_cnt;
+        s.sp_meta = p->sp.sp_meta;
+        s.sp_tile_row = p->sp.sp_tile_row;
+        const int pairs = (int)std::min<int64_t>(sms / 2, p->n_sp_units);
+        if (pairs > 0) {
+          spmm_tall2_sp_kernel<<<(unsigned)(2 * pairs), SP_THREADS, SMEM_SP, st>>>(p->tmSP, tmB, p->tmSPE, s);
+          RB_CUDA_TRY(cudaGetLastError());
+        }
+        if (p->n_res_items > 0) {  // C += residuals x B (groups of 4 with more than two nonzeros), same stream
+          SkinnyArgs kr{};
+          kr.row_perm = p->v.row_perm;
+          kr.items = p->d_res_items;
+          kr.n_items = p->n_res_items;
+          kr.B = B;
+          kr.ldb = ldb;
+          kr.C = C;
+          kr.ldc = ldc;
+          kr.N = (int32_t)p->N;
+          kr.accumulate = 1;
+          CsrArgs cr{p->sp.res_ptr, nullptr, nullptr, p->sp.res_col, p->sp.res_val};
+          return launch_csr(kr, cr, p->b_dtype, p->d_res_sched, st);
+        }
+        return (int)RB_OK;
+      }
+      SpmmArgs s = a;
+      s.items = p->d_items;
+      s.n_items = (int32_t)p->n_tall;
+      const int pairs = (int)std::min<int64_t>(sms / 2, p->n_tall);
+      spmm_tall2_kernel<<<(unsigned)(2 * pairs), TC_THREADS, SMEM_TALL, st>>>(p->tmA128, tmB, s);
       RB_CUDA_TRY(cudaGetLastError());
-    }
-    if (p->n_res_items > 0) {  // C += residuals x B (groups of 4 with more than two nonzeros)
-      SkinnyArgs k{};
-      k.row_perm = p->v.row_perm;
-      k.items = p->d_res_items;
-      k.n_items = p->n_res_items;
-      k.B = B;
-      k.ldb = ldb;
-      k.C = C;
-      k.ldc = ldc;
-      k.N = (int32_t)p->N;
-      k.accumulate = 1;
-      CsrArgs c{p->sp.res_ptr, nullptr, nullptr, p->sp.res_col, p->sp.res_val};
-      int rc = launch_csr(k, c, p->b_dtype, p->d_res_sched, stream);
-      if (rc) return rc;
-    }
-  } else if (p->n_tall > 0) {
-    a.items = p->d_items;
-    a.n_items = (int32_t)p->n_tall;
-    const int pairs = (int)std::min<int64_t>(sms / 2, p->n_tall);
-    spmm_tall2_kernel<<<(unsigned)(2 * pairs), TC_THREADS, SMEM_TALL, stream>>>(p->tmA128, tmB, a);
-    RB_CUDA_TRY(cudaGetLastError());
+      return (int)RB_OK;
+    });
+  if (p->b_dtype != RB_F32 && p->n_short > 0)
+    tasks.push_back([&](cudaStream_t st) {
+      SpmmArgs s = a;
+      s.items = p->d_items + 2 * p->n_tall;
+      s.n_items = (int32_t)p->n_short;
+      s.a_evict_first = 1;
+      const int ctas = (int)std::min<int64_t>(sms, p->n_short);
+      spmm_short2_kernel<<<(unsigned)ctas, TC_THREADS, SMEM_SHORT, st>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
+                                                                        tmB, s);
+      RB_CUDA_TRY(cudaGetLastError());
+      return (int)RB_OK;
+    });
+  if (tasks.size() <= 1) return tasks.empty() ? (int)RB_OK : tasks[0](stream);
+  // fork / join over auxiliary streams (created once per plan); the largest task stays on `stream`
+  if (!p->aux_ready) {
+    for (int l = 0; l < kAuxStreams; ++l) RB_CUDA_TRY(cudaStreamCreateWithFlags(&p->aux[l], cudaStreamNonBlocking));
+    for (int l = 0; l <= kAuxStreams; ++l) RB_CUDA_TRY(cudaEventCreateWithFlags(&p->ev[l], cudaEventDisableTiming));
+    p->aux_ready = true;
   }
-  if (p->n_short > 0) {
-    a.items = p->d_items + 2 * p->n_tall;
-    a.n_items = (int32_t)p->n_short;
-    a.a_evict_first = 1;
-    const int ctas = (int)std::min<int64_t>(sms, p->n_short);
-    spmm_short2_kernel<<<(unsigned)ctas, TC_THREADS, SMEM_SHORT, stream>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
-                                                                          tmB, a);
-    RB_CUDA_TRY(cudaGetLastError());
+  RB_CUDA_TRY(cudaEventRecord(p->ev[kAuxStreams], stream));
+  const int lanes = (int)std::min<size_t>(tasks.size(), kAuxStreams + 1);
+  for (int l = 1; l < lanes; ++l) RB_CUDA_TRY(cudaStreamWaitEvent(p->aux[l - 1], p->ev[kAuxStreams], 0));
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    const int l = (int)(i % lanes);
+    int rc = tasks[i](l == 0 ? stream : p->aux[l - 1]);
+    if (rc) return rc;
+  }
+  for (int l = 1; l < lanes; ++l) {
+    RB_CUDA_TRY(cudaEventRecord(p->ev[l - 1], p->aux[l - 1]));
+    RB_CUDA_TRY(cudaStreamWaitEvent(stream, p->ev[l - 1], 0));
   }
   return RB_OK;
 }
