@@ -77,6 +77,10 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+__device__ __forceinline__ void st_global_hint(float* p, float v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(policy) : "memory");
+}
+
 // 2-CTA (cta_group::2) TMA load: data lands in this CTA's smem, completion bytes are signalled on
 // the LEADER CTA's mbarrier (peer bit of the shared::cluster address cleared).
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <functional>
+#include <queue>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <vector>
@@ -73,6 +74,9 @@ struct SpmmArgs {
   int32_t N;
   uint32_t ab_fmt;      // 0 = f16, 1 = bf16
   uint32_t a_evict_first;  // L2 policy of A-tile loads: 1 = evict_first, 0 = evict_normal
+  uint32_t b_policy;       // short kernel B loads: 0 = evict_last, 1 = evict_normal, 2 = evict_first
+  uint32_t c_evict_first;  // short kernel C stores: 1 = L2 evict_first
+  const int32_t* cta_ptr;  // short kernel: items of CTA b are [cta_ptr[b], cta_ptr[b+1]) (null = round robin)
   int32_t short_ns;        // C columns per short item: 128 or 256
   float* ws;               // split-K partials of tall units: [slot][split][8 warps][8 chunks][32 cols][32 lanes]
   int32_t* cnt;            // split-K arrival counters: [slot][8 warps] (zero between launches)
@@ -86,6 +90,11 @@ struct SpmmArgs {
 // sums them in split order (deterministic: the sum order does not depend on arrival order).
 constexpr int MAX_SPLIT = 4;
 constexpr int WARP_PART = 8 * 32 * 32;  // floats of one epilogue warp's partial (32 rows x 256 cols)
+
+// Item range of this CTA: a precomputed per-CTA list (cta_ptr) or plain round robin.
+__device__ __forceinline__ int item_begin(const SpmmArgs& a) { return a.cta_ptr ? a.cta_ptr[blockIdx.x] : blockIdx.x; }
+__device__ __forceinline__ int item_end(const SpmmArgs& a) { return a.cta_ptr ? a.cta_ptr[blockIdx.x + 1] : a.n_items; }
+__device__ __forceinline__ int item_step(const SpmmArgs& a) { return a.cta_ptr ? 1 : (int)gridDim.x; }
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -619,9 +628,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmB);
       const uint64_t pol_a = a.a_evict_first ? policy_evict_first() : policy_evict_normal();
-      const uint64_t pol_b = policy_evict_last();
+      const uint64_t pol_b = a.b_policy == 0 ? policy_evict_last()
+                             : a.b_policy == 1 ? policy_evict_normal() : policy_evict_first();
       PipeState ps;
-      for (int i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+      for (int i = item_begin(a); i < item_end(a); i += item_step(a)) {
         const int4 it = a.items[i];
         const int g = it.x, hp = it.y, n0 = it.z;
         const CUtensorMap* tmA = hp == 16 ? &tmA16 : hp == 32 ? &tmA32 : hp == 64 ? &tmA64 : &tmA128;
@@ -654,7 +664,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       PipeState ps;
       int acc = 0;
       uint32_t aph = 0;
-      for (int i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+      for (int i = item_begin(a); i < item_end(a); i += item_step(a)) {
         const int4 it = a.items[i];
         const int g = it.x, hp = it.y, n0 = it.z;
         const int nk = (a.blk_ptr[g + 1] - a.blk_ptr[g]) * a.dp_chunks;
@@ -689,9 +699,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // epilogue: TMEM lane = C column, column = block-row row; a warp stores 32 consecutive floats
     // (128 B) of one C row per instruction
     const int q = warp & 3;
+    const uint64_t pol_c = policy_evict_first();
     int acc = 0;
     uint32_t aph = 0;
-    for (int i = blockIdx.x; i < a.n_items; i += gridDim.x) {
+    for (int i = item_begin(a); i < item_end(a); i += item_step(a)) {
       const int4 it = a.items[i];
       const int g = it.x, hp = it.y, n0 = it.z;
       const int p0 = a.row_partition[g];
@@ -717,7 +728,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (nvalid) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              if (j0 + j < h) a.C[(int64_t)a.row_perm[p0 + j0 + j] * a.ldc + n] = __uint_as_float(r[j]);
+              if (j0 + j < h) {
+                float* dst = a.C + (int64_t)a.row_perm[p0 + j0 + j] * a.ldc + n;
+                if (a.c_evict_first)
+                  st_global_hint(dst, __uint_as_float(r[j]), pol_c);
+                else
+                  *dst = __uint_as_float(r[j]);
+              }
             }
           }
         }
@@ -896,6 +913,8 @@ struct rb_spmm_plan {
   int64_t n_tall = 0, n_short = 0, n_simt = 0;
   rb::SkinnyItem* d_skinny = nullptr;  // skinny items, grouped by height class
   int32_t* d_zero = nullptr;            // permuted positions of rows in block rows without blocks
+  int32_t* d_short_ptr = nullptr;       // per-CTA ranges of the short items (short_schedule)
+  int32_t short_ctas = 0;
   int64_t n_zero = 0;
   std::vector<int4> tall_items;         // (g, m, n0, -) before K splitting (for the 2:4 re-plan)
   int64_t shard_lo = 0, shard_hi = 0;
@@ -993,6 +1012,41 @@ extern "C" int rb_spmm_shard_range(const int32_t* row_partition, const int32_t* 
                                    int64_t* row_end) {
   if (!row_partition || !blk_ptr || !row_begin || !row_end || n_block_rows < 0) return fail(RB_EINVAL, "bad arguments");
   return shard_range(row_partition, blk_ptr, n_block_rows, b_dtype, dp, shard, n_shards, row_begin, row_end);
+}
+
+// Static balanced schedule of the short items: list scheduling, in the given order, onto `ctas`
+// CTAs (each item goes to the CTA that frees up first under a bytes-per-K-step cost model); the
+// items are then regrouped CTA-contiguously and cta_ptr[b] .. cta_ptr[b+1] is CTA b's sequence.
+// Within one column slab the block rows go longest first, so the slab-major order that keeps the
+// B slab hot in L2 is kept while the partial last wave of every rank's shard is filled evenly.
+static void short_schedule(std::vector<int4>& items, int ctas, int dpc, bool slab_major,
+                           std::vector<int32_t>& cta_ptr) {
+  if (slab_major)
+    std::stable_sort(items.begin(), items.end(), [](const int4& x, const int4& y) {
+      return x.z != y.z ? x.z < y.z : x.w > y.w;
+    });
+  // cost in 8 KB units: per K step 4 B boxes + the hp x 64 tile; per item ~2 units of setup
+  std::vector<double> fin(ctas, 0.0);
+  std::vector<int32_t> owner(items.size());
+  using E = std::pair<double, int>;
+  std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
+  for (int c = 0; c < ctas; ++c) heap.push({0.0, c});
+  std::vector<int32_t> count(ctas, 0);
+  for (size_t i = 0; i < items.size(); ++i) {
+    const int4& it = items[i];
+    const double cost = (double)it.w * dpc * (4.0 + it.y / 64.0) + 2.0;
+    E top = heap.top();
+    heap.pop();
+    owner[i] = top.second;
+    ++count[top.second];
+    heap.push({top.first + cost, top.second});
+  }
+  cta_ptr.assign(ctas + 1, 0);
+  for (int c = 0; c < ctas; ++c) cta_ptr[c + 1] = cta_ptr[c] + count[c];
+  std::vector<int4> out(items.size());
+  std::vector<int32_t> pos(cta_ptr.begin(), cta_ptr.end() - 1);
+  for (size_t i = 0; i < items.size(); ++i) out[pos[owner[i]]++] = items[i];
+  items.swap(out);
 }
 
 extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
@@ -1116,6 +1170,9 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   std::vector<int4> tall_units;
   int64_t n_slots = 0;
   split_tail(tall, sms / 2, tall_units, n_slots);
+  std::vector<int32_t> short_ptr;
+  const int short_ctas = (int)std::min<int64_t>(sms, (int64_t)shrt.size());
+  if (short_ctas > 0) short_schedule(shrt, short_ctas, dpc, !short_g_major, short_ptr);
 
   auto* p = new rb_spmm_plan();
   p->v = *vbr;
@@ -1194,6 +1251,18 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
     if (rc) {
       rb_spmm_plan_destroy(p);
       return rc;
+    }
+  }
+  if (short_ctas > 0) {
+    p->short_ctas = short_ctas;
+    cudaError_t e = cudaMalloc(&p->d_short_ptr, sizeof(int32_t) * short_ptr.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_short_ptr, short_ptr.data(), sizeof(int32_t) * short_ptr.size(),
+                          cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "short schedule");
     }
   }
   if (!zero_rows.empty()) {
@@ -1322,6 +1391,7 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_skinny_cnt) cudaFree(p->d_skinny_cnt);
   if (p->d_sched) cudaFree(p->d_sched);
   if (p->d_zero) cudaFree(p->d_zero);
+  if (p->d_short_ptr) cudaFree(p->d_short_ptr);
   if (p->d_sp_units) cudaFree(p->d_sp_units);
   if (p->d_sp_ws) cudaFree(p->d_sp_ws);
   if (p->d_sp_cnt) cudaFree(p->d_sp_cnt);
@@ -1354,6 +1424,9 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.N = (int32_t)p->N;
   a.ab_fmt = p->b_dtype == RB_BF16 ? 1u : 0u;
   a.a_evict_first = 0;
+  a.b_policy = 0;
+  a.c_evict_first = 0;
+  a.cta_ptr = nullptr;
   a.short_ns = p->short_ns;
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
@@ -1471,7 +1544,13 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
       s.items = p->d_items + 2 * p->n_tall;
       s.n_items = (int32_t)p->n_short;
       s.a_evict_first = 1;
-      const int ctas = (int)std::min<int64_t>(sms, p->n_short);
+      if (const char* e = std::getenv("RB_SHORT_CACHE")) {  // experiment knob: "<a><b><c>" digits
+        if (e[0]) s.a_evict_first = e[0] == '1';
+        if (e[0] && e[1]) s.b_policy = (uint32_t)(e[1] - '0') % 3;
+        if (e[0] && e[1] && e[2]) s.c_evict_first = e[2] == '1';
+      }
+      s.cta_ptr = p->d_short_ptr;
+      const int ctas = p->short_ctas;
       spmm_short2_kernel<<<(unsigned)ctas, TC_THREADS, SMEM_SHORT, st>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
                                                                         tmB, s);
       RB_CUDA_TRY(cudaGetLastError());
