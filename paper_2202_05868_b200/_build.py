@@ -22,6 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["capi.cu", "spmm.cu", "spmm_skinny.cu", "vbr_build.cu", "blocking.cu", "stats.cu", "csr.cu", "sparse24.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+FLAGS += os.environ.get("RB_EXTRA_NVCC_FLAGS", "").split()  # developer builds (e.g. -DRB_PROF_1SA)
 
 
 def _deps_mtime() -> float:

@@ -734,7 +734,7 @@ SWs carve_sparse(void* base, int64_t n, int64_t nnz, int64_t n_seg) {
   w.cand_ok = (uint8_t*)take(3 * n1);
   w.seed_item = (int32_t*)take(4 * n1);
   w.ctrl = (int32_t*)take(4 * (16 + 2 * kSparseBlocks));
-  w.stats = (unsigned long long*)take(8 * 8);
+  w.stats = (unsigned long long*)take(8 * 24);
   w.scratch = (int32_t*)take(4 * (size_t)kSparseBlocks * 3 * (s1 + 1));
   w.pcnt = (int64_t*)take(8 * (n1 + 1));
   w.b32 = (int32_t*)take(4 * s1);
@@ -1075,15 +1075,46 @@ __device__ __forceinline__ int64_t item_inter(const SGreedyArgs& a, const unsign
   return inter;
 }
 
+// Candidates with more segments than this are intersected by a whole warp (deferred through a
+// shared queue), so one thread never walks a hub item's long list alone while the block (and, in a
+// GROUP round, the grid barrier) waits for it.
+constexpr int64_t kWarpItem = 32;
+
+// warp-cooperative |P ∩ segs(j)| (all lanes return the total)
+__device__ __forceinline__ int64_t warp_item_inter(const SGreedyArgs& a, const unsigned long long* sP, int64_t p0,
+                                                   int64_t p1) {
+  const int lane = threadIdx.x & 31;
+  int cnt = 0;
+  for (int64_t p = p0 + lane; p < p1; p += 32) {
+    const int32_t sg = __ldg(a.item_seg + p);
+    cnt += (int)((sP[sg >> 6] >> (sg & 63)) & 1ull);
+  }
+  return (int64_t)__reduce_add_sync(0xffffffffu, cnt);
+}
+
 // Merge verdict for candidate j.  accept_dev is non-decreasing in inter and inter <= min(psize, size),
 // so a candidate that fails even with inter = min(psize, size) is rejected without reading its list.
-__device__ __forceinline__ bool eval_candidate(const SGreedyArgs& a, const unsigned long long* sP, int32_t j,
-                                               int64_t psize, double cap, bool* grows) {
+// Returns 1 = accepted, 0 = rejected, -1 = deferred (passes the size pre-check and has more than
+// kWarpItem segments: the caller queues it for warp_eval).
+__device__ __forceinline__ int eval_candidate(const SGreedyArgs& a, const unsigned long long* sP, int32_t j,
+                                              int64_t psize, double cap, bool* grows) {
   const int64_t p0 = __ldg(a.item_ptr + j), p1 = __ldg(a.item_ptr + j + 1);
   const int64_t sz = p1 - p0;
   *grows = false;
-  if (!accept_dev(min(psize, sz), psize, sz, a.tau, a.cosine, a.bounded, cap)) return false;
+  if (!accept_dev(min(psize, sz), psize, sz, a.tau, a.cosine, a.bounded, cap)) return 0;
+  if (sz > kWarpItem) return -1;
   const int64_t inter = item_inter(a, sP, p0, p1);
+  const bool ok = accept_dev(inter, psize, sz, a.tau, a.cosine, a.bounded, cap);
+  *grows = ok && a.update && inter < sz;
+  return ok ? 1 : 0;
+}
+
+// Warp verdict for a deferred candidate (all lanes get the same answer).
+__device__ __forceinline__ bool warp_eval(const SGreedyArgs& a, const unsigned long long* sP, int32_t j,
+                                          int64_t psize, double cap, bool* grows) {
+  const int64_t p0 = __ldg(a.item_ptr + j), p1 = __ldg(a.item_ptr + j + 1);
+  const int64_t sz = p1 - p0;
+  const int64_t inter = warp_item_inter(a, sP, p0, p1);
   const bool ok = accept_dev(inter, psize, sz, a.tau, a.cosine, a.bounded, cap);
   *grows = ok && a.update && inter < sz;
   return ok;
@@ -1105,6 +1136,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
   __shared__ int32_t s_list_len, s_f, s_js;
   __shared__ int32_t s_mode, s_next, s_gnext, s_seed, s_g, s_pos, s_psize, s_rid, s_batch;
   __shared__ int32_t s_acc_list, s_acc_cnt, s_acc_limit, s_acc_g;
+  __shared__ int32_t s_defer[kSparseThreads], s_ndefer;  // large candidates for warp_eval
   __shared__ int32_t s_bpos, s_blen, s_grounds;  // batch cursor / length, rounds of the current group
   __shared__ double s_cap;
 
@@ -1155,19 +1187,29 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
       int32_t* flags = a.ctrl + 16 + (batch & 1) * kSparseBlocks;
       const int32_t my = (int32_t)blockIdx.x < len ? s_list[blockIdx.x] : -1;
       if (my >= 0) {
+#ifdef RB_PROF_1SA
+        const long long c0 = clock64();
+#endif
         const int32_t psize = load_pattern(a, sP, pl, s_psize, my);
         if (threadIdx.x == 0) {
           s_psize = psize;
           bs.flag = 0;
         }
         __syncthreads();
+#ifdef RB_PROF_1SA
+        const long long c1 = clock64();
+#endif
         const double cap = __ddiv_rn((double)psize, cap_den);
         int mode;
         int32_t emp_lo;
         const int64_t total = prepare_round(a, pl, bs, psize, my + 1, &mode, &emp_lo);
+#ifdef RB_PROF_1SA
+        const long long c2 = clock64();
+#endif
         // a seed with a large candidate set is not tested speculatively by one CTA: reporting "unknown"
         // (treated as a hit) ends the singleton run here and the GROUP protocol (all CTAs) takes it
         if (total > a.batch_max_enum && threadIdx.x == 0) bs.flag = 2;
+        if (threadIdx.x == 0) s_ndefer = 0;
         __syncthreads();
         for (int64_t e0 = 0; e0 < total && !bs.flag; e0 += blockDim.x) {
           const int64_t e = e0 + threadIdx.x;
@@ -1175,19 +1217,52 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
             const int32_t j = entry_item(a, pl, mode, psize, e, my + 1, emp_lo);
             if (__ldcg(a.group_of_item + j) < 0) {
               bool grows;
-              if (eval_candidate(a, sP, j, psize, cap, &grows)) bs.flag = 1;
+              const int v = eval_candidate(a, sP, j, psize, cap, &grows);
+              if (v > 0) bs.flag = 1;
+              else if (v < 0) s_defer[atomicAdd(&s_ndefer, 1)] = j;
             }
           }
           __syncthreads();
+          const int32_t nd = s_ndefer;
+          if (!bs.flag && nd > 0) {
+            for (int32_t k = threadIdx.x >> 5; k < nd; k += blockDim.x >> 5) {
+              bool grows;
+              if (warp_eval(a, sP, s_defer[k], psize, cap, &grows) && lane == 0) bs.flag = 1;
+            }
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) s_ndefer = 0;
           if (bs.flag) break;  // uniform: read after the barrier
         }
         if (threadIdx.x == 0) flags[blockIdx.x] = bs.flag;
+#ifdef RB_PROF_1SA
+        if (threadIdx.x == 0) {
+          const long long c3 = clock64();
+          atomicAdd(a.stats + 8, (unsigned long long)(c1 - c0));
+          atomicAdd(a.stats + 9, (unsigned long long)(c2 - c1));
+          atomicAdd(a.stats + 10, (unsigned long long)(c3 - c2));
+          atomicAdd(a.stats + 11, (unsigned long long)total);
+          atomicMax(a.stats + 12 + (batch & 1), (unsigned long long)(c3 - t_phase));
+          atomicMax(a.stats + 16 + (batch & 1), (unsigned long long)psize);
+          if (bs.flag == 2) atomicAdd(a.stats + 15, 1ull);
+        }
+#endif
       }
+#ifdef RB_PROF_1SA
+      const long long cb = clock64();
+#endif
       grid_barrier(a.ctrl + 8, a.ctrl + 9);
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.stats[0] += 1;
         a.stats[1] += len;
         a.stats[5] += clock64() - t_phase;
+#ifdef RB_PROF_1SA
+        a.stats[14] += a.stats[12 + (batch & 1)];
+        a.stats[12 + (batch & 1)] = 0;
+        a.stats[18] += clock64() - cb;
+        a.stats[19] += a.stats[16 + (batch & 1)];
+        a.stats[16 + (batch & 1)] = 0;
+#endif
       }
       if (threadIdx.x == 0) {
         s_bpos = 0;
@@ -1286,33 +1361,54 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
     {
       int32_t* cj = a.cand_j + (size_t)slot * m;
       uint8_t* co = a.cand_ok + (size_t)slot * m;
-      for (int64_t e0 = 0; e0 < total; e0 += gthreads) {
-        const int64_t e = e0 + gtid;
+      if (threadIdx.x == 0) s_ndefer = 0;
+      __syncthreads();
+      for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < total; e0 += gthreads) {  // uniform per block
+        const int64_t e = e0 + threadIdx.x;
         bool has = false, ok = false;
         int32_t j = -1;
         if (e < total) {
           j = entry_item(a, pl, mode, psize, e, pos, emp_lo);
           if (__ldcg(a.group_of_item + j) < 0 && (mode == 2 || atomicExch(a.stamp + j, rid) != rid)) {
-            has = true;
             bool grows;
-            ok = eval_candidate(a, sP, j, psize, cap, &grows);
-            my_ok += ok ? 1 : 0;
-            if (grows) my_js = min(my_js, j);
+            const int v = eval_candidate(a, sP, j, psize, cap, &grows);
+            if (v < 0) {
+              s_defer[atomicAdd(&s_ndefer, 1)] = j;
+            } else {
+              has = true;
+              ok = v > 0;
+              my_ok += ok ? 1 : 0;
+              if (grows) my_js = min(my_js, j);
+            }
           }
         }
-        const unsigned act = __activemask();
-        const unsigned ball = __ballot_sync(act, has);
+        const unsigned ball = __ballot_sync(0xffffffffu, has);
         if (ball) {
-          const int leader = __ffs(act) - 1;
           int32_t base = 0;
-          if (lane == leader) base = atomicAdd(a.ctrl + 3 + slot, __popc(ball));
-          base = __shfl_sync(act, base, leader);
+          if (lane == 0) base = atomicAdd(a.ctrl + 3 + slot, __popc(ball));
+          base = __shfl_sync(0xffffffffu, base, 0);
           if (has) {
             const int32_t idx = base + __popc(ball & ((1u << lane) - 1u));
             cj[idx] = j;
             co[idx] = ok ? 1 : 0;
           }
         }
+        __syncthreads();
+        const int32_t nd = s_ndefer;
+        for (int32_t k = threadIdx.x >> 5; k < nd; k += blockDim.x >> 5) {  // warp per large candidate
+          const int32_t jd = s_defer[k];
+          bool grows;
+          const bool okd = warp_eval(a, sP, jd, psize, cap, &grows);
+          if (lane == 0) {
+            const int32_t idx = atomicAdd(a.ctrl + 3 + slot, 1);
+            cj[idx] = jd;
+            co[idx] = okd ? 1 : 0;
+            my_ok += okd ? 1 : 0;
+            if (grows) my_js = min(my_js, jd);
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_ndefer = 0;
       }
     }
     my_js = __reduce_min_sync(0xffffffffu, my_js);
@@ -1512,7 +1608,7 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     ga.stats = ws.stats;
     ga.batch_max_enum = kBatchMaxEnumDefault;
     if (const char* e = std::getenv("RB_1SA_BATCH_ENUM")) ga.batch_max_enum = std::max<int64_t>(0, std::atoll(e));
-    RB_CUDA_TRY(cudaMemsetAsync(ws.stats, 0, 8 * 8, stream));
+    RB_CUDA_TRY(cudaMemsetAsync(ws.stats, 0, 8 * 24, stream));
     const size_t shm = sizeof(uint64_t) * W + sizeof(int32_t) * 3 * kPlistSmem;
     if (shm > 200 * 1024) return fail(RB_EUNSUPPORTED, "too many segments for the pattern bitset in shared memory");
     void* fn = (void*)sparse_greedy_kernel;
@@ -1540,6 +1636,15 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     fprintf(stderr, "[rb 1sa sparse] m=%d H=%lld batches=%llu seeds=%llu singletons=%llu rounds=%llu accepts=%llu "
             "batch_Mcyc=%.1f group_Mcyc=%.1f\n", m, (long long)H, st[0], st[1], st[2], st[3], st[4], st[5] / 1e6,
             st[6] / 1e6);
+#ifdef RB_PROF_1SA
+    unsigned long long pf[24];
+    RB_CUDA_TRY(cudaMemcpy(pf, ws.stats, sizeof(pf), cudaMemcpyDeviceToHost));
+    const double seeds = std::max(1.0, (double)pf[1]), batches = std::max(1.0, (double)pf[0]);
+    fprintf(stderr, "[rb 1sa prof] per seed: load %.0f prep %.0f enum %.0f cyc, entries %.0f; per batch: max CTA "
+            "%.0f cyc, block0 barrier wait %.0f cyc, max psize %.0f; punted seeds %llu\n", pf[8] / seeds,
+            pf[9] / seeds, pf[10] / seeds, pf[11] / seeds, pf[14] / batches, pf[18] / batches, pf[19] / batches,
+            pf[15]);
+#endif
   }
   // ---- assembly (as the dense path)
   assembly_keys_kernel<<<g1, 256, 0, stream>>>(ws.item_of_row, ws.group_of_item, n, m, ws.keys_a, ws.vals_a);
