@@ -670,10 +670,12 @@ struct SWs {
   int32_t* n_empty;        // [1]
   int32_t* group_of_item;  // [n]
   int32_t* stamp;          // [n]
+  int32_t* sstamp;         // [n] speculative-test dedupe stamps
   int32_t* cand_j;         // [3*n]
   uint8_t* cand_ok;        // [3*n]
   int32_t* seed_item;      // [n]
-  int32_t* ctrl;           // [16 + 2*blocks]
+  int32_t* ctrl;           // [16 + 4*blocks]
+  int64_t* htotal;         // [blocks] candidate-set sizes of the punted seeds of a batch
   unsigned long long* stats;  // [8]
   int32_t* scratch;        // [blocks * 3 * (n_seg+1)]
   int64_t* pcnt;           // [n+1]
@@ -730,10 +732,12 @@ SWs carve_sparse(void* base, int64_t n, int64_t nnz, int64_t n_seg) {
   w.n_empty = (int32_t*)take(16);
   w.group_of_item = (int32_t*)take(4 * n1);
   w.stamp = (int32_t*)take(4 * n1);
+  w.sstamp = (int32_t*)take(4 * n1);
   w.cand_j = (int32_t*)take(4 * 3 * n1);
   w.cand_ok = (uint8_t*)take(3 * n1);
   w.seed_item = (int32_t*)take(4 * n1);
-  w.ctrl = (int32_t*)take(4 * (16 + 2 * kSparseBlocks));
+  w.ctrl = (int32_t*)take(4 * (16 + 4 * kSparseBlocks));
+  w.htotal = (int64_t*)take(8 * kSparseBlocks);
   w.stats = (unsigned long long*)take(8 * 24);
   w.scratch = (int32_t*)take(4 * (size_t)kSparseBlocks * 3 * (s1 + 1));
   w.pcnt = (int64_t*)take(8 * (n1 + 1));
@@ -889,15 +893,20 @@ struct SGreedyArgs {
   int32_t cosine, bounded, update;
   int32_t* group_of_item;
   int32_t* stamp;
+  int32_t* sstamp;   // [m] speculative tests: id of the last (batch, seed) test that claimed the item
   int32_t* cand_j;   // [3][m]
   uint8_t* cand_ok;  // [3][m]
   int32_t* seed_item;
   int32_t* ctrl;     // [0..2] first growing hit, [3..5] candidate counts, [6] H, [8] count, [9] gen,
-                     // [10..12] accepted-candidate counts, [16..16+2*kSparseBlocks) speculative flags
+                     // [10..12] accepted-candidate counts, [16..16+2*kSparseBlocks) speculative flags,
+                     // [16+2*kSparseBlocks..16+4*kSparseBlocks) HEAVY verdicts of punted seeds
   int32_t* scratch;  // per block: overflow of the pattern list arrays, 3 x (n_seg+1)
   unsigned long long* stats;  // [8] counters (block 0): batches, batch seeds, singletons, rounds, accepts,
-                              //     cycles in BATCH, cycles in GROUP, batch-skips
+                              //     cycles in BATCH, cycles in GROUP, HEAVY passes
   int64_t batch_max_enum;
+  int64_t* htotal;   // [kSparseBlocks] candidate-set size of each punted seed of the current batch
+  int32_t heavy;     // resolve punted seeds with all CTAs in one pass (HEAVY phase)
+  int64_t heavy_max_enum;  // entries one HEAVY pass may enumerate (the punted seeds that fit, in order)
 };
 
 constexpr int kPlistSmem = 4096;
@@ -905,6 +914,9 @@ constexpr int kPlistSmem = 4096;
 // candidate sets go to the all-CTA GROUP round.  24 x 512 measured best on config 3 (R-MAT 2^20):
 // tau 0.7 3.60 -> 2.08 s, 0.3 6.51 -> 5.95 s vs 4 x 512 (RB_1SA_BATCH_ENUM overrides).
 constexpr int64_t kBatchMaxEnumDefault = 24 * kSparseThreads;
+// A HEAVY pass resolves, in batch order, the punted seeds whose candidate sets fit this many entries
+// in total (the rest still go to GROUP rounds).  A hit on seed k stops the work on every later seed.
+constexpr int64_t kHeavyMaxEnumDefault = 2 << 20;
 
 // The pattern's segment list and its prefix-enumeration arrays (start, exclusive-scan of lengths).
 struct PList {
@@ -1120,6 +1132,51 @@ __device__ __forceinline__ bool warp_eval(const SGreedyArgs& a, const unsigned l
   return ok;
 }
 
+// Speculative test of a seed over its enumeration entries [e_lo, e_hi): bs.flag becomes 1 at the
+// first accepted candidate (bs.flag must be 0 on entry).  `stop` (optional) is polled every
+// iteration: another CTA already found a hit for this seed.
+// Returns true iff this CTA itself found an accepted candidate.
+__device__ bool spec_enumerate(const SGreedyArgs& a, const unsigned long long* sP, PList& pl, BlockShared& bs,
+                               int mode, int32_t psize, int32_t pos, int32_t emp_lo, double cap, int64_t e_lo,
+                               int64_t e_hi, int32_t* s_defer, int32_t* s_ndefer, int32_t sid,
+                               const int32_t* stop, const int32_t* stop_min = nullptr, int32_t my_k = 0) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) *s_ndefer = 0;
+  __syncthreads();
+  for (int64_t e0 = e_lo; e0 < e_hi; e0 += blockDim.x) {
+    const int64_t e = e0 + threadIdx.x;
+    if (e < e_hi) {
+      const int32_t j = entry_item(a, pl, mode, psize, e, pos, emp_lo);
+      // an item listed under several prefix segments is tested once per (batch, seed): `sid`
+      if (__ldcg(a.group_of_item + j) < 0 && (mode == 2 || atomicExch(a.sstamp + j, sid) != sid)) {
+        bool grows;
+        const int v = eval_candidate(a, sP, j, psize, cap, &grows);
+        if (v > 0) bs.flag = 1;
+        else if (v < 0) s_defer[atomicAdd(s_ndefer, 1)] = j;
+      }
+    }
+    __syncthreads();
+    const int32_t nd = *s_ndefer;
+    if (!bs.flag && nd > 0) {
+      for (int32_t k = threadIdx.x >> 5; k < nd; k += blockDim.x >> 5) {
+        bool grows;
+        if (warp_eval(a, sP, s_defer[k], psize, cap, &grows) && lane == 0) bs.flag = 1;
+      }
+    }
+    // stop early (flag 3, not a hit of ours): another CTA found a hit for this seed or an earlier one
+    if (threadIdx.x == 0 && !bs.flag && stop &&
+        (*((volatile const int32_t*)stop) || (stop_min && *((volatile const int32_t*)stop_min) < my_k)))
+      bs.flag = 3;
+    __syncthreads();
+    if (threadIdx.x == 0) *s_ndefer = 0;
+    if (bs.flag) break;  // uniform: read after the barrier
+  }
+  __syncthreads();
+  const bool found = bs.flag == 1;
+  __syncthreads();
+  return found;
+}
+
 // The greedy scan with speculative singleton batching (exact):
 //  BATCH: every CTA b takes the b-th unassigned item >= next as a speculative seed and tests whether
 //         ANY later unassigned item passes the merge test against it.  Seeds before the first one that
@@ -1137,6 +1194,8 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
   __shared__ int32_t s_mode, s_next, s_gnext, s_seed, s_g, s_pos, s_psize, s_rid, s_batch;
   __shared__ int32_t s_acc_list, s_acc_cnt, s_acc_limit, s_acc_g;
   __shared__ int32_t s_defer[kSparseThreads], s_ndefer;  // large candidates for warp_eval
+  __shared__ int64_t s_pre[kSparseBlocks + 1];            // HEAVY: prefix of the punted totals
+  __shared__ int32_t s_f1, s_fh;  // first definite hit of the batch; end of the HEAVY-resolved prefix
   __shared__ int32_t s_bpos, s_blen, s_grounds;  // batch cursor / length, rounds of the current group
   __shared__ double s_cap;
 
@@ -1185,6 +1244,9 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
       if (len == 0) break;
       const int32_t batch = s_batch;
       int32_t* flags = a.ctrl + 16 + (batch & 1) * kSparseBlocks;
+      int32_t* hres = a.ctrl + 16 + (2 + (batch & 1)) * kSparseBlocks;
+      int32_t* hmin = a.ctrl + 13 + (batch & 1);  // earliest seed index with a HEAVY hit
+      if (blockIdx.x == 0 && threadIdx.x == 0) *hmin = INT_MAX;
       const int32_t my = (int32_t)blockIdx.x < len ? s_list[blockIdx.x] : -1;
       if (my >= 0) {
 #ifdef RB_PROF_1SA
@@ -1206,35 +1268,19 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
 #ifdef RB_PROF_1SA
         const long long c2 = clock64();
 #endif
-        // a seed with a large candidate set is not tested speculatively by one CTA: reporting "unknown"
-        // (treated as a hit) ends the singleton run here and the GROUP protocol (all CTAs) takes it
-        if (total > a.batch_max_enum && threadIdx.x == 0) bs.flag = 2;
-        if (threadIdx.x == 0) s_ndefer = 0;
-        __syncthreads();
-        for (int64_t e0 = 0; e0 < total && !bs.flag; e0 += blockDim.x) {
-          const int64_t e = e0 + threadIdx.x;
-          if (e < total) {
-            const int32_t j = entry_item(a, pl, mode, psize, e, my + 1, emp_lo);
-            if (__ldcg(a.group_of_item + j) < 0) {
-              bool grows;
-              const int v = eval_candidate(a, sP, j, psize, cap, &grows);
-              if (v > 0) bs.flag = 1;
-              else if (v < 0) s_defer[atomicAdd(&s_ndefer, 1)] = j;
-            }
+        // a seed with a large candidate set is not tested by one CTA: it is punted (flag 2) and, if it
+        // precedes the batch's first definite hit, resolved by the HEAVY pass below with all CTAs
+        if (total > a.batch_max_enum) {
+          if (threadIdx.x == 0) {
+            a.htotal[blockIdx.x] = total;
+            hres[blockIdx.x] = 0;
+            flags[blockIdx.x] = 2;
           }
-          __syncthreads();
-          const int32_t nd = s_ndefer;
-          if (!bs.flag && nd > 0) {
-            for (int32_t k = threadIdx.x >> 5; k < nd; k += blockDim.x >> 5) {
-              bool grows;
-              if (warp_eval(a, sP, s_defer[k], psize, cap, &grows) && lane == 0) bs.flag = 1;
-            }
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) s_ndefer = 0;
-          if (bs.flag) break;  // uniform: read after the barrier
+        } else {
+          spec_enumerate(a, sP, pl, bs, mode, psize, my + 1, emp_lo, cap, 0, total, s_defer, &s_ndefer,
+                         batch * kSparseBlocks + (int32_t)blockIdx.x + 1, nullptr);
+          if (threadIdx.x == 0) flags[blockIdx.x] = bs.flag;
         }
-        if (threadIdx.x == 0) flags[blockIdx.x] = bs.flag;
 #ifdef RB_PROF_1SA
         if (threadIdx.x == 0) {
           const long long c3 = clock64();
@@ -1244,7 +1290,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
           atomicAdd(a.stats + 11, (unsigned long long)total);
           atomicMax(a.stats + 12 + (batch & 1), (unsigned long long)(c3 - t_phase));
           atomicMax(a.stats + 16 + (batch & 1), (unsigned long long)psize);
-          if (bs.flag == 2) atomicAdd(a.stats + 15, 1ull);
+          if (total > a.batch_max_enum) atomicAdd(a.stats + 15, 1ull);
         }
 #endif
       }
@@ -1264,6 +1310,79 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
         a.stats[16 + (batch & 1)] = 0;
 #endif
       }
+      // ============================ HEAVY: the punted seeds before the first definite hit, all
+      // candidate sets concatenated and cut evenly over the CTAs (one pass, one barrier)
+      if (threadIdx.x == 0) s_f1 = len;
+      __syncthreads();
+      for (int32_t k = threadIdx.x; k < len; k += blockDim.x)
+        if (*((volatile const int32_t*)(flags + k)) == 1) atomicMin(&s_f1, k);
+      __syncthreads();
+      const int32_t f1 = s_f1;
+      {
+        // s_pre[k] = exclusive prefix of the punted totals (k < f1), s_pre[len] = total
+        for (int32_t k = threadIdx.x; k < kSparseBlocks + 1; k += blockDim.x) s_pre[k] = 0;
+        __syncthreads();
+        if (a.heavy)
+          for (int32_t k = threadIdx.x; k < f1; k += blockDim.x)
+            if (*((volatile const int32_t*)(flags + k)) == 2) s_pre[k + 1] = __ldcg(a.htotal + k);
+        __syncthreads();
+        if (threadIdx.x == 0) {  // include punted seeds in order while the pass stays within budget
+          int32_t fh = f1;
+          for (int32_t k = 1; k <= len; ++k) {
+            if (k - 1 >= fh || s_pre[k - 1] + s_pre[k] > a.heavy_max_enum) {
+              if (k - 1 < fh && s_pre[k] > 0) fh = k - 1;
+              s_pre[k] = s_pre[k - 1];
+            } else {
+              s_pre[k] += s_pre[k - 1];
+            }
+          }
+          s_fh = fh;
+        }
+        __syncthreads();
+      }
+      const int64_t T_all = s_pre[len];
+      if (T_all > 0) {
+        const int64_t c_lo = T_all * blockIdx.x / gridDim.x, c_hi = T_all * (blockIdx.x + 1) / gridDim.x;
+        for (int32_t k = 0; k < s_fh; ++k) {  // block-uniform
+          const int64_t k_lo = s_pre[k], k_hi = s_pre[k + 1];
+          if (k_hi <= k_lo || k_hi <= c_lo || k_lo >= c_hi) continue;
+          // another CTA may set hres[k] at any time: one thread reads it, the block follows
+          if (threadIdx.x == 0)
+            bs.flag = *((volatile const int32_t*)(hres + k)) || *((volatile const int32_t*)hmin) < k;
+          __syncthreads();
+          const bool done = bs.flag != 0;
+          __syncthreads();
+          if (done) continue;
+          const int32_t seed = s_list[k];
+          const int32_t psize = load_pattern(a, sP, pl, s_psize, seed);
+          if (threadIdx.x == 0) {
+            s_psize = psize;
+            bs.flag = 0;
+          }
+          __syncthreads();
+          const double cap = __ddiv_rn((double)psize, cap_den);
+          int mode;
+          int32_t emp_lo;
+          prepare_round(a, pl, bs, psize, seed + 1, &mode, &emp_lo);
+          if (threadIdx.x == 0) bs.flag = 0;
+          __syncthreads();
+          const bool found = spec_enumerate(a, sP, pl, bs, mode, psize, seed + 1, emp_lo, cap,
+                                            max(c_lo, k_lo) - k_lo, min(c_hi, k_hi) - k_lo, s_defer, &s_ndefer,
+                                            batch * kSparseBlocks + k + 1, hres + k, hmin, k);
+          if (threadIdx.x == 0 && found) {
+            hres[k] = 1;
+            atomicMin(hmin, k);
+          }
+        }
+        grid_barrier(a.ctrl + 8, a.ctrl + 9);
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.stats[7] += 1;
+        // the earliest resolved hit ends the resolved prefix: seeds after it may have been cut short
+        if (threadIdx.x == 0) {
+          const int32_t hm = *((volatile const int32_t*)hmin);
+          if (hm != INT_MAX) s_fh = min(s_fh, hm + 1);
+        }
+        __syncthreads();
+      }
       if (threadIdx.x == 0) {
         s_bpos = 0;
         s_blen = len;
@@ -1277,11 +1396,16 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_greedy_kernel(SGreedyAr
       // CTA reads the same flags and commits nothing that any CTA reads again)
       const int32_t len = s_blen, bpos = s_bpos;
       const int32_t* flags = a.ctrl + 16 + ((s_batch - 1) & 1) * kSparseBlocks;
+      const int32_t* hres = a.ctrl + 16 + (2 + ((s_batch - 1) & 1)) * kSparseBlocks;
+      const int32_t f1 = s_fh;  // punted seeds before this index were resolved by the HEAVY pass
       if (threadIdx.x < 32) {
         int32_t f = len;
         for (int32_t k0 = bpos; k0 < len; k0 += 32) {
           const int32_t k = k0 + lane;
-          const bool hit = k < len && *((volatile const int32_t*)(flags + k)) != 0;
+          int32_t v = k < len ? *((volatile const int32_t*)(flags + k)) : 0;
+          // a punted seed before the first definite hit was resolved by the HEAVY pass (if enabled)
+          if (v == 2 && a.heavy && k < f1) v = *((volatile const int32_t*)(hres + k));
+          const bool hit = v != 0;
           const unsigned b = __ballot_sync(0xffffffffu, hit);
           if (b) {
             f = k0 + __ffs(b) - 1;
@@ -1580,7 +1704,7 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
   RB_CUDA_TRY(cudaGetLastError());
   // ---- K3: pruned greedy scan
   {
-    std::vector<int32_t> ctrl0(16 + 2 * kSparseBlocks, 0);
+    std::vector<int32_t> ctrl0(16 + 4 * kSparseBlocks, 0);
     for (int i = 0; i < 3; ++i) ctrl0[i] = INT_MAX;
     RB_CUDA_TRY(cudaMemcpyAsync(ws.ctrl, ctrl0.data(), sizeof(int32_t) * ctrl0.size(), cudaMemcpyHostToDevice, stream));
     SGreedyArgs ga;
@@ -1600,6 +1724,8 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     ga.update = pattern_update != 0;
     ga.group_of_item = ws.group_of_item;
     ga.stamp = ws.stamp;
+    ga.sstamp = ws.sstamp;
+    RB_CUDA_TRY(cudaMemsetAsync(ws.sstamp, 0, sizeof(int32_t) * std::max<int64_t>(m, 1), stream));
     ga.cand_j = ws.cand_j;
     ga.cand_ok = ws.cand_ok;
     ga.seed_item = ws.seed_item;
@@ -1607,6 +1733,11 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     ga.scratch = ws.scratch;
     ga.stats = ws.stats;
     ga.batch_max_enum = kBatchMaxEnumDefault;
+    ga.htotal = ws.htotal;
+    ga.heavy = 1;
+    if (const char* e = std::getenv("RB_1SA_HEAVY")) ga.heavy = e[0] != '0';
+    ga.heavy_max_enum = kHeavyMaxEnumDefault;
+    if (const char* e = std::getenv("RB_1SA_HEAVY_ENUM")) ga.heavy_max_enum = std::max<int64_t>(0, std::atoll(e));
     if (const char* e = std::getenv("RB_1SA_BATCH_ENUM")) ga.batch_max_enum = std::max<int64_t>(0, std::atoll(e));
     RB_CUDA_TRY(cudaMemsetAsync(ws.stats, 0, 8 * 24, stream));
     const size_t shm = sizeof(uint64_t) * W + sizeof(int32_t) * 3 * kPlistSmem;
@@ -1634,8 +1765,8 @@ int block_1sa_sparse(int64_t n, int64_t nnz, const int64_t* row_ptr, const int64
     unsigned long long st[8];
     RB_CUDA_TRY(cudaMemcpy(st, ws.stats, sizeof(st), cudaMemcpyDeviceToHost));
     fprintf(stderr, "[rb 1sa sparse] m=%d H=%lld batches=%llu seeds=%llu singletons=%llu rounds=%llu accepts=%llu "
-            "batch_Mcyc=%.1f group_Mcyc=%.1f\n", m, (long long)H, st[0], st[1], st[2], st[3], st[4], st[5] / 1e6,
-            st[6] / 1e6);
+            "batch_Mcyc=%.1f group_Mcyc=%.1f heavy_passes=%llu\n", m, (long long)H, st[0], st[1], st[2], st[3], st[4],
+            st[5] / 1e6, st[6] / 1e6, st[7]);
 #ifdef RB_PROF_1SA
     unsigned long long pf[24];
     RB_CUDA_TRY(cudaMemcpy(pf, ws.stats, sizeof(pf), cudaMemcpyDeviceToHost));

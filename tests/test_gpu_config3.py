@@ -27,6 +27,17 @@ def test_rmat_block_1sa_matches_pruned_oracle(scale, tau):
     assert np.array_equal(dg.pattern_idx[: pp[-1]].cpu().numpy(), ref["pattern_idx"])
 
 
+@pytest.mark.parametrize("batch_enum,heavy_enum", [("0", "2097152"), ("64", "3000"), ("256", "0")])
+@pytest.mark.parametrize("scale,tau", [(64, 0.3), (16, 0.5)])
+def test_rmat_block_1sa_heavy_pass_matches_pruned_oracle(scale, tau, batch_enum, heavy_enum, monkeypatch):
+    """Speculative seeds too large for one CTA are punted and resolved by the all-CTA HEAVY pass
+    (or, past its budget, by GROUP rounds).  Forcing tiny caps routes most seeds through those paths;
+    the grouping must stay bit-exact."""
+    monkeypatch.setenv("RB_1SA_BATCH_ENUM", batch_enum)
+    monkeypatch.setenv("RB_1SA_HEAVY_ENUM", heavy_enum)
+    test_rmat_block_1sa_matches_pruned_oracle(scale, tau)
+
+
 def _digest(t):
     import hashlib
 
