@@ -1145,7 +1145,9 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
     for (int c = 0; c < SKINNY_CLASSES; ++c) {
       const int nb_batch = std::max(2, 32 / skinny_class_h(c));  // blocks per staged batch (LPR / H)
       const int64_t want = (cls_blocks[c] + target - 1) / std::max<int64_t>(target, 1);
-      part[c] = (int)std::min<int64_t>(SKINNY_PART_BLOCKS, std::max<int64_t>(2 * nb_batch, want));
+      int min_batches = 1;
+      if (const char* e = std::getenv("RB_SKINNY_MIN_BATCHES")) min_batches = std::max(1, std::atoi(e));
+      part[c] = (int)std::min<int64_t>(SKINNY_PART_BLOCKS, std::max<int64_t>(min_batches * nb_batch, want));
     }
     for (const int2& r : skinny_rows) {
       const int h = rp[r.x + 1] - rp[r.x];
