@@ -213,6 +213,23 @@ def host_csr(dA):
     return (dA.row_ptr.cpu().numpy(), dA.col_idx.cpu().numpy(), dA.values.cpu().numpy())
 
 
+def host_info():
+    """The CPU the baseline ran on (model, cpu_count, affinity, BLAS threads)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        affinity = None
+    blas = {k: os.environ[k] for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS") if k in os.environ}
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": affinity, "blas_env": blas,
+            "numpy": np.__version__}
+
+
 def cpu_baseline(dA, bounds, dv, B, target_seconds, threads):
     """Calibrate on a small sample, then time a sample sized for ~target_seconds."""
     A_host = host_csr(dA)
@@ -228,7 +245,7 @@ def cpu_baseline(dA, bounds, dv, B, target_seconds, threads):
     t = time_cpu(s, bounds, B64, threads)
     useful = 2.0 * s["nnz"] * N
     return {"value": useful / t / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "seconds": t,
+            "seconds": t, "host": host_info(),
             "sample": f"oracle.spmm_vbr_np (numpy port of multiply.py:72-97, float64, per-block dgemm, "
                       f"threads={threads}) on the first {s['rows']} permuted rows ({s['block_rows']} block rows, "
                       f"{s['nnz']} nnz) of the same VBR structure and B"}
@@ -456,7 +473,7 @@ def run_reference(args, world, rank):
            "config": {"workload": f"config {cfg.name}: {cfg.description}", "n_rows": dA.n_rows, "n_cols": dA.n_cols,
                       "nnz": dA.nnz, "N": cfg.N, "delta": cfg.delta, "tau": cfg.tau},
            "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                            "sample": desc},
+                            "sample": desc, "host": host_info()},
            "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
