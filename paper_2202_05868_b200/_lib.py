@@ -12,7 +12,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librowblock_b200.so")
+LIB_PATH = os.environ.get("ROWBLOCK_B200_LIB") or os.path.join(HERE, "librowblock_b200.so")  # override: experiments
 
 RB_OK, RB_EINVAL, RB_ECUDA, RB_ENOMEM, RB_EUNSUPPORTED = 0, 1, 2, 3, 4
 RB_F32, RB_BF16, RB_F16, RB_F64 = 0, 1, 2, 3

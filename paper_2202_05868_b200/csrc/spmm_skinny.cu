@@ -203,6 +203,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// h = 1 class: B gathers in flight per lane and resident CTAs per SM (developer overrides)
+#ifndef RB_SK1_DEPTH
+#define RB_SK1_DEPTH 6
+#endif
+#ifndef RB_SK1_MINB
+#define RB_SK1_MINB 5
+#endif
 constexpr int STAGED_WARPS = 4;  // 128-thread CTAs: 5 resident per SM (registers <= 102, 41 KB smem each)
 
 template <typename T, int LPR>
@@ -216,55 +223,89 @@ struct SkinnySmem {
   static constexpr int CTA_BYTES = STAGED_WARPS * (32 / LPR) * GROUP_BYTES;
 };
 
+// Per-item constants of the staged path and the two operations that start a batch: the lane's
+// block metadata (first B row k0 and width w of block bb + gl) and the cp.async staging of the
+// batch's tile rows.  They are free functions so the kernel can start the NEXT item's first batch
+// while the current item's last batch is still gathering (the item chain no longer pays the
+// metadata + staging latency in series).
+template <typename T>
+struct StagedCtx {
+  int g, p0, h, b0, hp, bb, be;
+  const T* tiles;
+};
+template <typename T>
+__device__ __forceinline__ StagedCtx<T> staged_ctx(const SkinnyArgs& a, const SkinnyItem& it) {
+  StagedCtx<T> c;
+  c.g = it.g;
+  c.p0 = a.row_partition[it.g];
+  c.h = a.row_partition[it.g + 1] - c.p0;
+  c.b0 = a.blk_ptr[it.g];
+  c.hp = hp_of(c.h);
+  c.bb = it.bb;
+  c.be = it.be;
+  c.tiles = static_cast<const T*>(a.tiles) + a.grp_tile_row[it.g] * (int64_t)a.dp;
+  return c;
+}
+template <typename T, int H, int LPR>
+__device__ __forceinline__ void staged_meta(const SkinnyArgs& a, const StagedCtx<T>& c, int bb, int gl, int& k0,
+                                            int& w) {
+  constexpr int NB = LPR / H;
+  k0 = 0;
+  w = 0;
+  if (gl < NB && gl < c.be - bb) {
+    const int bc = __ldg(a.blk_col + bb + gl);
+    k0 = __ldg(a.col_bounds + bc);
+    w = __ldg(a.col_bounds + bc + 1) - k0;
+  }
+}
+template <typename T, int H, int LPR>
+__device__ __forceinline__ void staged_issue(const SkinnyArgs& a, const StagedCtx<T>& c, int bb, uint8_t* buf,
+                                             int w_lane, int gl, unsigned gmask) {
+  using S = SkinnySmem<T, LPR>;
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int NB = LPR / H;
+  const int nbb = min(NB, c.be - bb);
+  const int64_t dp = a.dp;
+#pragma unroll
+  for (int t = 0; t < S::PPB; ++t) {
+    const int q = t * LPR + gl;
+    const int row = q / S::PPB, pc = q - row * S::PPB;  // staged row = j * H + r
+    const int j = row / H, r = row - j * H;
+    const int wj = __shfl_sync(gmask, w_lane, j, LPR);
+    const bool pred = j < nbb && r < c.h && pc * VEC < wj;
+    cp_async16(buf + row * S::ROW + pc * 16,
+               pred ? c.tiles + ((int64_t)(bb - c.b0 + j) * c.hp + r) * dp + pc * VEC : c.tiles, pred);
+  }
+  cp_async_commit();
+}
+
 // Block rows of height h <= H (H = 1, 2, 4, 8), tiles at most 64 columns wide.  Per batch of
 // NB = LPR / H blocks the lane group
 //   * stages the blocks' h tile rows in shared memory with cp.async (double buffered: the next
-//     batch's rows and block columns are in flight while this batch's B rows are gathered),
+//     batch's rows and block columns are in flight while this batch's B rows are gathered; during
+//     the item's last batch, the next item's first batch is),
 //   * lane j turns block j's staged rows into the 64-bit mask of columns holding a nonzero in any
 //     row (16-byte shared loads, padded rows),
 //   * a group prefix sum orders those columns (block ascending, k ascending) into a list,
 //   * the list is streamed with DEPTH B-row gathers in flight per lane; each gathered B row feeds
 //     all h accumulators, the tile values coming from shared memory (broadcast reads).
+// On entry the item's first batch is already staged in stage[buf] with metadata (k0c, wc); `next`
+// (when has_next) is started in the other buffer during the last batch, and buf / k0c / wc / cnext
+// are left describing it.
 template <typename T, int H, int LPR, bool ALIGNED>
-__device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyItem& it, int cols, int gl,
-                                            unsigned gmask, uint8_t* stage, int2* list) {
+__device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyItem& it, const StagedCtx<T>& c,
+                                            int cols, int gl, unsigned gmask, uint8_t* stage, int2* list,
+                                            int& buf, int& k0c, int& wc, bool has_next, const SkinnyItem& next,
+                                            StagedCtx<T>& cnext) {
   using S = SkinnySmem<T, LPR>;
   constexpr int VEC = 16 / sizeof(T);
   constexpr int NB = LPR / H;                 // blocks per batch
-  constexpr int DEPTH = H >= 4 ? 4 : H == 1 ? 6 : 8;  // B gathers in flight per lane
+  constexpr int DEPTH = H >= 4 ? 4 : H == 1 ? RB_SK1_DEPTH : 8;  // B gathers in flight per lane
   constexpr int ROWE = S::ROW / (int)sizeof(T);
-  const int g = it.g;
   const int n = it.n0 + gl * VEC;
-  const int p0 = a.row_partition[g], h = a.row_partition[g + 1] - p0;
-  const int b0 = a.blk_ptr[g];
-  const int hp = hp_of(h);
-  const int64_t dp = a.dp, ldb = a.ldb;
-  const T* tiles = static_cast<const T*>(a.tiles) + a.grp_tile_row[g] * dp;
+  const int h = c.h;
+  const int64_t ldb = a.ldb;
   const T* Bn = static_cast<const T*>(a.B) + n;
-
-  auto meta = [&](int bb, int& k0, int& w) {
-    k0 = 0;
-    w = 0;
-    if (gl < NB && gl < it.be - bb) {
-      const int bc = __ldg(a.blk_col + bb + gl);
-      k0 = __ldg(a.col_bounds + bc);
-      w = __ldg(a.col_bounds + bc + 1) - k0;
-    }
-  };
-  auto stage_issue = [&](int bb, uint8_t* buf, int w_lane) {
-    const int nbb = min(NB, it.be - bb);
-#pragma unroll
-    for (int t = 0; t < S::PPB; ++t) {
-      const int q = t * LPR + gl;
-      const int row = q / S::PPB, pc = q - row * S::PPB;  // staged row = j * H + r
-      const int j = row / H, r = row - j * H;
-      const int wj = __shfl_sync(gmask, w_lane, j, LPR);
-      const bool pred = j < nbb && r < h && pc * VEC < wj;
-      cp_async16(buf + row * S::ROW + pc * 16,
-                 pred ? tiles + ((int64_t)(bb - b0 + j) * hp + r) * dp + pc * VEC : tiles, pred);
-    }
-    cp_async_commit();
-  };
 
   float acc[H][VEC];
 #pragma unroll
@@ -272,15 +313,17 @@ __device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyIte
 #pragma unroll
     for (int e = 0; e < VEC; ++e) acc[r][e] = 0.f;
 
-  int k0c, wc;
-  meta(it.bb, k0c, wc);
-  stage_issue(it.bb, stage, wc);
-  int buf = 0;
   for (int bb = it.bb; bb < it.be; bb += NB, buf ^= 1) {
     const int nbb = min(NB, it.be - bb);
     const int bbn = bb + NB;
+    const bool last = bbn >= it.be;
     int k0n = 0, wn = 0;
-    if (bbn < it.be) meta(bbn, k0n, wn);  // in flight while this batch is processed
+    if (!last) {
+      staged_meta<T, H, LPR>(a, c, bbn, gl, k0n, wn);  // in flight while this batch is processed
+    } else if (has_next) {
+      cnext = staged_ctx<T>(a, next);
+      staged_meta<T, H, LPR>(a, cnext, next.bb, gl, k0n, wn);
+    }
     uint8_t* cur = stage + buf * S::STAGE;
     const T* curT = reinterpret_cast<const T*>(cur);
     cp_async_wait_all();
@@ -320,6 +363,10 @@ __device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyIte
     const int total = __shfl_sync(gmask, incl, LPR - 1, LPR);
     const int excl = incl - cnt;
     bool issued = false;
+    auto issue_next = [&]() {  // the next batch's (or the next item's first) rows land while this one gathers
+      if (!last) staged_issue<T, H, LPR>(a, c, bbn, stage + (buf ^ 1) * S::STAGE, wn, gl, gmask);
+      else if (has_next) staged_issue<T, H, LPR>(a, cnext, next.bb, stage + (buf ^ 1) * S::STAGE, wn, gl, gmask);
+    };
     for (int base = 0; base < total; base += S::CAP) {
       if (excl < base + S::CAP && incl > base) {
         uint64_t m = msk;
@@ -335,8 +382,8 @@ __device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyIte
         }
       }
       __syncwarp(gmask);
-      if (!issued && bbn < it.be) {  // next batch's rows land while this window's B rows are gathered
-        stage_issue(bbn, stage + (buf ^ 1) * S::STAGE, wn);
+      if (!issued) {
+        issue_next();
         issued = true;
       }
       const int nh = min(S::CAP, total - base);
@@ -364,15 +411,20 @@ __device__ __forceinline__ void staged_item(const SkinnyArgs& a, const SkinnyIte
       }
       __syncwarp(gmask);
     }
-    if (!issued && bbn < it.be) stage_issue(bbn, stage + (buf ^ 1) * S::STAGE, wn);
+    if (!issued) issue_next();
     k0c = k0n;
     wc = wn;
   }
-  skinny_finish<H, VEC, LPR, ALIGNED>(a, it, cols, h, p0, n, gl, gmask, acc);
+  if (it.bb >= it.be && has_next) {  // empty item: start the next one in the current buffer
+    cnext = staged_ctx<T>(a, next);
+    staged_meta<T, H, LPR>(a, cnext, next.bb, gl, k0c, wc);
+    staged_issue<T, H, LPR>(a, cnext, next.bb, stage + buf * S::STAGE, wc, gl, gmask);
+  }
+  skinny_finish<H, VEC, LPR, ALIGNED>(a, it, cols, h, c.p0, n, gl, gmask, acc);
 }
 
 template <typename T, int H, int LPR, bool ALIGNED>
-__global__ void __launch_bounds__(STAGED_WARPS * 32, H == 1 ? 5 : 2) spmm_skinny_staged_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
+__global__ void __launch_bounds__(STAGED_WARPS * 32, H == 1 ? RB_SK1_MINB : 2) spmm_skinny_staged_kernel(SkinnyArgs a, int cols, unsigned long long* sched) {
   using S = SkinnySmem<T, LPR>;
   constexpr int GPW = 32 / LPR;
   extern __shared__ uint4 smem_sk[];
@@ -380,10 +432,24 @@ __global__ void __launch_bounds__(STAGED_WARPS * 32, H == 1 ? 5 : 2) spmm_skinny
   const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
   uint8_t* gbase = reinterpret_cast<uint8_t*>(smem_sk) + (warp * GPW + grp) * S::GROUP_BYTES;
   int2* list = reinterpret_cast<int2*>(gbase + 2 * S::STAGE);
-  for (;;) {
-    const int64_t i = next_item<LPR>(sched, gl, gmask);
-    if (i >= a.n_items) break;
-    staged_item<T, H, LPR, ALIGNED>(a, load_item(a.items + i), cols, gl, gmask, gbase, list);
+  const int64_t i0 = next_item<LPR>(sched, gl, gmask);
+  if (i0 < a.n_items) {
+    SkinnyItem it = load_item(a.items + i0);
+    StagedCtx<T> c = staged_ctx<T>(a, it);
+    int buf = 0, k0c, wc;
+    staged_meta<T, H, LPR>(a, c, it.bb, gl, k0c, wc);
+    staged_issue<T, H, LPR>(a, c, it.bb, gbase, wc, gl, gmask);
+    for (;;) {
+      // claim the next item now; it is needed only when this item's last batch starts
+      const int64_t inext = next_item<LPR>(sched, gl, gmask);
+      const bool has_next = inext < a.n_items;
+      const SkinnyItem next = has_next ? load_item(a.items + inext) : it;
+      StagedCtx<T> cnext = c;
+      staged_item<T, H, LPR, ALIGNED>(a, it, c, cols, gl, gmask, gbase, list, buf, k0c, wc, has_next, next, cnext);
+      if (!has_next) break;
+      it = next;
+      c = cnext;
+    }
   }
   leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
 }
