@@ -526,3 +526,30 @@ def test_spmm_sparse24_tall_matches_product(density, N, delta):
     bound = np.abs(Ad) @ np.abs(Bh)
     assert_close(C1.cpu().numpy().astype(np.float64), Ad @ Bh, bound, 1e-4, "sparse24")
     assert_close(Cd.cpu().numpy().astype(np.float64), Ad @ Bh, bound, 1e-4, "dense")
+
+
+@pytest.mark.parametrize("precision,world", [("bf16", 2), ("bf16", 3), ("bf16", 8), ("fp32", 3)])
+def test_spmm_shard_plans_cover_rows_and_match_full(precision, world):
+    """bench.py --gpus W runs shard k of W on rank k (rb_spmm_plan_create(shard, n_shards)).  Running
+    every shard's plan on one device into one C must write every row (NaN-initialised C) and match
+    the single-plan product within fp32 reassociation (tall tails are split differently per shard)."""
+    from paper_2202_05868_b200 import _lib as L
+    from paper_2202_05868_b200.device import DeviceCsr, DeviceVbr
+
+    rng = np.random.default_rng(31 + world)
+    heights = [1, 3, 6, 20, 64, 90, 130, 300, 1, 2, 517] * 2  # skinny, short and tall block rows
+    A, perm, rp = _grouped_matrix(rng, heights, 1536, 64, 0.02)
+    q = rb.ColumnPartition.uniform(1536, 64)
+    dt = L.TORCH_DTYPE[L.PRECISION[precision]]
+    N = 384
+    Bh = rounded(rng.uniform(-1, 1, (1536, N)), dt if dt != torch.float32 else torch.bfloat16)
+    Bd = torch.from_numpy(Bh).to(dt).cuda()
+    dv = DeviceVbr.build(DeviceCsr.from_host(A, "cuda"), q, perm, rp, dtypes=(precision,))
+    full = dv.spmm(Bd, precision=precision)
+    C = torch.full_like(full, float("nan"))
+    for k in range(world):
+        dv.spmm(Bd, out=C, precision=precision, shard=k, n_shards=world)
+    torch.cuda.synchronize()
+    assert not torch.isnan(C).any(), "a row was not written by any shard"
+    err = (C.double() - full.double()).abs().max().item()
+    assert err <= 1e-5 * max(1.0, full.abs().max().item())
