@@ -26,6 +26,12 @@ __host__ __device__ inline int32_t hp_of(int32_t h) {
   return (h + 127) / 128 * 128;
 }
 __host__ __device__ inline bool is_short_row(int32_t h) { return h <= 128; }
+// Row pitch of a block row's tiles in the tile array: block rows of h <= 8 rows (CUDA-core skinny
+// kernels; config 3 / 2b are almost all h = 1) store exactly h rows per tile instead of hp = 16, so
+// their tiles are 16x smaller and contiguous.  The swap-AB tensor-core kernel, when it does take
+// such a block row, reads hp rows from the pitch-spaced start: rows h..hp-1 then belong to the next
+// tiles (or are TMA zero fill) and only feed accumulator rows the epilogue never stores.
+__host__ __device__ inline int32_t tile_pitch(int32_t h) { return h <= 8 ? h : hp_of(h); }
 
 // Thread-local error string for rb_last_error_string().
 void set_error(const std::string& s);

@@ -638,6 +638,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int b_begin = a.blk_ptr[g];
         const int nk = (a.blk_ptr[g + 1] - b_begin) * a.dp_chunks;
         const int64_t row0 = a.grp_tile_row[g];
+        const int pitch = tile_pitch(a.row_partition[g + 1] - a.row_partition[g]);
         const int n_boxes = min(a.short_ns / 64, (a.N - n0 + 63) / 64);
         const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
         for (int k = 0; k < nk; ++k) {
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int bcol = a.blk_col[b_begin + t];
           uint8_t* sA = smem + ps.s * S_STAGE;
           uint8_t* sB = sA + S_A_SLOT;
-          tma_load_2d_hint(sA, tmA, &full[ps.s], kc * KCH, (int32_t)(row0 + (int64_t)t * hp), pol_a);
+          tma_load_2d_hint(sA, tmA, &full[ps.s], kc * KCH, (int32_t)(row0 + (int64_t)t * pitch), pol_a);
           const int krow = a.col_bounds[bcol] + kc * KCH;
           for (int bx = 0; bx < n_boxes; ++bx)
             tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[ps.s], n0 + 64 * bx, krow, pol_b);
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, co
   const int g = it.x, r0 = it.y, n0 = it.z;
   const int p0 = a.row_partition[g];
   const int h = a.row_partition[g + 1] - p0;
-  const int hp = hp_of(h);
+  const int hp = tile_pitch(h);  // tile row pitch
   const int rows = min(SIMT_ROWS, h - r0);
   const int n = n0 + threadIdx.x;
   const bool nv = n < a.N;

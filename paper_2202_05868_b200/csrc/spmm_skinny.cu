@@ -240,7 +240,7 @@ __device__ __forceinline__ StagedCtx<T> staged_ctx(const SkinnyArgs& a, const Sk
   c.p0 = a.row_partition[it.g];
   c.h = a.row_partition[it.g + 1] - c.p0;
   c.b0 = a.blk_ptr[it.g];
-  c.hp = hp_of(c.h);
+  c.hp = tile_pitch(c.h);  // tile row pitch
   c.bb = it.bb;
   c.be = it.be;
   c.tiles = static_cast<const T*>(a.tiles) + a.grp_tile_row[it.g] * (int64_t)a.dp;
@@ -466,7 +466,7 @@ __device__ __forceinline__ void skinny_item(const SkinnyArgs& a, const SkinnyIte
   const int n = it.n0 + gl * VEC;
   const int p0 = a.row_partition[g], h = a.row_partition[g + 1] - p0;
   const int b0 = a.blk_ptr[g];
-  const int hp = hp_of(h);
+  const int hp = tile_pitch(h);  // tile row pitch
   const int64_t dp = a.dp, ldb = a.ldb;
   const T* tiles = static_cast<const T*>(a.tiles) + a.grp_tile_row[g] * dp;
   const T* B = static_cast<const T*>(a.B) + n;

@@ -170,7 +170,7 @@ __global__ void count_kernel(const unsigned long long* __restrict__ gbits, int64
     if (lane == 0) {
       blk_cnt[g] = running;
       const int32_t h = (int32_t)(row_partition[g + 1] - row_partition[g]);
-      tile_cnt[g] = (int64_t)running * hp_of(h);
+      tile_cnt[g] = (int64_t)running * tile_pitch(h);
     }
   }
 }
@@ -216,7 +216,7 @@ __global__ void scatter_kernel(const int64_t* __restrict__ row_ptr, const int64_
     if (s1 == s0) continue;
     const int32_t g = group_of_row[r];
     const int32_t local = pos_of_row[r] - rpart[g];
-    const int32_t hp = hp_of(rpart[g + 1] - rpart[g]);
+    const int32_t hp = tile_pitch(rpart[g + 1] - rpart[g]);  // row pitch of this block row's tiles
     const int64_t base = grp_tile_row[g];
     const unsigned long long* gb = gbits + (int64_t)g * W;
     const int32_t* wp = wprefix + (int64_t)g * W;

@@ -35,6 +35,11 @@ def _i64(x, device) -> torch.Tensor:
     return host_tensor(np.asarray(x, dtype=np.int64)).to(device)
 
 
+def tile_pitch(h: int) -> int:
+    """Row pitch of a block row's tiles (mirrors csrc/common.cuh tile_pitch): h for h <= 8, else hp_of."""
+    return h if h <= 8 else hp_of(h)
+
+
 def hp_of(h: int) -> int:
     """Padded tile height (mirrors csrc/common.cuh hp_of)."""
     if h <= 16:
@@ -172,8 +177,9 @@ class DeviceVbr:
     """VBR matrix resident in HBM.
 
     Structure (int32): row_partition[H+1], row_perm[n], blk_ptr[H+1], blk_col[nb],
-    grp_tile_row[H] (int64), col_bounds[n_seg+1].  Tiles: block t of block row g is an
-    hp(h_g) x dp row-major tile at tile row grp_tile_row[g] + t*hp(h_g); one tile array per dtype.
+    grp_tile_row[H] (int64), col_bounds[n_seg+1].  Tiles: block t of block row g is a
+    row-major tile of h_g valid rows x dp at tile row grp_tile_row[g] + t*pitch(h_g), pitch = h_g
+    for h_g <= 8 else hp(h_g) (zero padding rows); one tile array per dtype.
     """
 
     def __init__(self):
@@ -389,7 +395,7 @@ class DeviceVbr:
         out = []
         for g in range(self.n_block_rows):
             h = int(rp[g + 1] - rp[g])
-            hp = hp_of(h)
+            hp = tile_pitch(h)
             base = int(tr[g])
             out.append(tuple(VbrBlock(int(bc[k]), tiles[base + (k - bp[g]) * hp: base + (k - bp[g]) * hp + h,
                                                           : int(widths[bc[k]])])
