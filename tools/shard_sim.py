@@ -41,4 +41,9 @@ for W in worlds:
     ts = [time_shard(k, W) for k in range(W)]
     out["worlds"][W] = {"max_ms": round(max(ts), 4), "min_ms": round(min(ts), 4),
                         "efficiency": round(t1 / (W * max(ts)), 4)}
+    if "-v" in sys.argv:
+        for k in range(W):
+            info = dv.plan_info(cfg.N, cfg.precision, k, W)
+            print(W, k, round(ts[k], 4), {f: info[f] for f in ("n_items_tall", "n_items_short", "n_items_skinny",
+                                                                 "executed_flops", "row_begin_perm")}, flush=True)
 print(json.dumps(out))
