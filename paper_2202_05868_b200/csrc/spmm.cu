@@ -1148,7 +1148,13 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       const int64_t want = (cls_blocks[c] + target - 1) / std::max<int64_t>(target, 1);
       int min_batches = 1;
       if (const char* e = std::getenv("RB_SKINNY_MIN_BATCHES")) min_batches = std::max(1, std::atoi(e));
-      part[c] = (int)std::min<int64_t>(SKINNY_PART_BLOCKS, std::max<int64_t>(min_batches * nb_batch, want));
+      // A shard holds 1/n_shards of the work but still a whole hub row: R-MAT hub rows are ~20x denser
+      // per block than the average skinny row, so at 4+ ranks their 256-block parts become the
+      // critical path (config 3, 8 ranks: 0.76 -> 0.48 ms with 64-block parts).  One GPU keeps 256
+      // (smaller parts cost more reduction than they save there).
+      int part_max = n_shards >= 8 ? SKINNY_PART_BLOCKS / 4 : n_shards >= 4 ? SKINNY_PART_BLOCKS / 2 : SKINNY_PART_BLOCKS;
+      if (const char* e = std::getenv("RB_SKINNY_PART_MAX")) part_max = std::max(1, std::atoi(e));
+      part[c] = (int)std::min<int64_t>(part_max, std::max<int64_t>(min_batches * nb_batch, want));
     }
     for (const int2& r : skinny_rows) {
       const int h = rp[r.x + 1] - rp[r.x];
