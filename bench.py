@@ -1,6 +1,6 @@
 """Benchmark: VBR SpMM effective GFLOP/s (2·nnz·N/s) on B200 vs the CPU reference path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
 One "step" = one pass of the hot path's SpMM over the whole synthetic workload
 (C = A·B with A resident as VBR tiles in HBM, B resident, C written in HBM).
@@ -14,7 +14,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import sys
 import threading
@@ -35,7 +34,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", default="2")
+    p.add_argument("--config", default="5")
     p.add_argument("--scale", type=int, default=1)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
@@ -154,39 +153,60 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------- CPU baseline
 
 
-def cpu_sample(A_host, bounds, row_perm, row_partition, group_width, N, target_flops):
-    """A bounded prefix of the permuted rows (whole block rows, the last one truncated) as a
-    standalone VBR problem for the oracle port of spmm_vbr (multiply.py:72-97).
-    group_width[g] = total stored-segment width of block row g (VBR-padded flops/row = 2*width*N)."""
+def reference_workload(name: str, scale: int, n_chunks: int):
+    """The reference's CPU path on this config, built WITHOUT the GPU library: host CSR
+    (synth.make_host: identical arrays to the GPU arm's), 1-SA by the C oracle (blocking.py:283-306),
+    stored blocks and float64 payloads by the C oracle (vbr.py:88-125), B as float64.  The block rows
+    are cut into ``n_chunks`` contiguous chunks of about equal VBR work; one timed step of the
+    reference arm multiplies one chunk with the numpy restatement of spmm_vbr (multiply.py:72-97), so
+    K steps over K chunks compute the whole product exactly once."""
+    import oracle
+    from paper_2202_05868_b200 import synth
+
+    t0 = time.perf_counter()
+    rp, ci, vals, bounds, cfg = synth.make_host(name, scale=scale)
+    t1 = time.perf_counter()
+    s = oracle.block_1sa_arrays(rp, ci, bounds, tau=cfg.tau, pruned=(name == "3"))
+    perm, gp = s["row_perm"], s["group_ptr"]
+    bp, bc = oracle.vbr_blocks(rp, ci, bounds, perm, gp)
+    t2 = time.perf_counter()
+    pay = oracle.vbr_payloads(rp, ci, vals, bounds, perm, gp, bp, bc)
+    t3 = time.perf_counter()
+    B = synth.make_b(cfg, len(bounds) and int(bounds[-1]), cfg.precision, device="cpu")
+    B64 = B.float().numpy().astype(np.float64)
+    n_rows, nnz, N = len(rp) - 1, int(rp[-1]), cfg.N
+    # chunks of contiguous block rows, cut on the prefix sum of VBR-padded work (h * stored width)
+    work = np.diff(np.asarray(gp, np.int64)) * group_widths(bounds, gp, bp, bc)
+    cw = np.concatenate([[0], np.cumsum(work)])
+    H = len(gp) - 1
+    cuts = np.searchsorted(cw, np.linspace(0, cw[-1], n_chunks + 1), side="left")
+    cuts[0], cuts[-1] = 0, H
+    cuts = np.maximum.accumulate(cuts)
+    row_nnz = np.diff(np.asarray(rp, np.int64))[np.asarray(perm, np.int64)]
+    rn = np.concatenate([[0], np.cumsum(row_nnz)])
+    gp64 = np.asarray(gp, np.int64)
+    chunks = [(int(cuts[k]), int(cuts[k + 1]), int(rn[gp64[cuts[k + 1]]] - rn[gp64[cuts[k]]]))
+              for k in range(n_chunks)]
+    return dict(cfg=cfg, payloads=pay, row_perm=perm, row_partition=gp, bounds=bounds, B64=B64, n_rows=n_rows,
+                n_cols=int(bounds[-1]), nnz=nnz, N=N, chunks=chunks, n_groups=H, n_blocks=len(bc),
+                setup={"synth_host_s": round(t1 - t0, 2), "oracle_1sa_vbr_s": round(t2 - t1, 2),
+                       "oracle_payloads_s": round(t3 - t2, 2)})
+
+
+def time_chunk(w, k, threads, C):
+    """One chunk of spmm_vbr (numpy restatement, multiply.py:72-97) -> seconds, useful flops."""
     import oracle
 
-    rp_ptr, cols, vals = A_host
-    rp = np.asarray(row_partition, np.int64)
-    perm = np.asarray(row_perm, np.int64)
-    flops, P, cuts = 0.0, 0, [0]
-    for g in range(len(rp) - 1):
-        h = int(rp[g + 1] - rp[g])
-        per_row = 2.0 * max(1, int(group_width[g])) * N
-        take = h
-        if flops + per_row * take > target_flops:
-            take = max(1, int((target_flops - flops) / per_row))
-        P += take
-        cuts.append(P)
-        flops += per_row * take
-        if take < h or flops >= target_flops:
-            break
-    sel = perm[:P]
-    counts = rp_ptr[sel + 1] - rp_ptr[sel]
-    sp = np.zeros(P + 1, np.int64)
-    np.cumsum(counts, out=sp[1:])
-    idx = np.repeat(rp_ptr[sel] - sp[:-1], counts) + np.arange(int(sp[-1]))
-    s_cols, s_vals = cols[idx], vals[idx]
-    s_perm = np.arange(P)
-    s_rp = np.asarray(cuts, np.int64)
-    bp, bc = oracle.vbr_blocks(sp, s_cols, bounds, s_perm, s_rp)
-    pay = oracle.vbr_payloads(sp, s_cols, s_vals, bounds, s_perm, s_rp, bp, bc)
-    return dict(payloads=pay, row_perm=s_perm, row_partition=s_rp, nnz=int(len(s_cols)), rows=P,
-                block_rows=len(cuts) - 1)
+    from threadpoolctl import threadpool_limits
+
+    lo, hi, nnz = w["chunks"][k]
+    # one BLAS thread per worker thread: `threads` Python workers each calling a multi-threaded
+    # OpenBLAS oversubscribe the cores (measured 7 vs 34 GFLOP/s on 8 cores, config 5 at 1/4 scale)
+    with threadpool_limits(limits=1, user_api="blas"):
+        t0 = time.perf_counter()
+        oracle.spmm_vbr_np(w["payloads"], w["row_perm"], w["row_partition"], w["bounds"], w["B64"], threads=threads,
+                           block_rows=range(lo, hi), out=C)
+        return time.perf_counter() - t0, 2.0 * nnz * w["N"]
 
 
 def group_widths(bounds, row_partition, blk_ptr, blk_col):
@@ -195,22 +215,6 @@ def group_widths(bounds, row_partition, blk_ptr, blk_col):
     per_blk = w[np.asarray(blk_col, np.int64)] if len(blk_col) else np.zeros(0, np.int64)
     cs = np.concatenate([[0], np.cumsum(per_blk)])
     return cs[bp[1:]] - cs[bp[:-1]]
-
-
-def time_cpu(sample, bounds, B64, threads, repeats=1):
-    import oracle
-
-    best = math.inf
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        oracle.spmm_vbr_np(sample["payloads"], sample["row_perm"], sample["row_partition"], bounds, B64,
-                           threads=threads)
-        best = min(best, time.perf_counter() - t0)
-    return best
-
-
-def host_csr(dA):
-    return (dA.row_ptr.cpu().numpy(), dA.col_idx.cpu().numpy(), dA.values.cpu().numpy())
 
 
 def host_info():
@@ -227,28 +231,25 @@ def host_info():
         affinity = None
     blas = {k: os.environ[k] for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS") if k in os.environ}
     return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": affinity, "blas_env": blas,
-            "numpy": np.__version__}
+            "blas_threads_per_worker": 1, "numpy": np.__version__}
 
 
-def cpu_baseline(dA, bounds, dv, B, target_seconds, threads):
-    """Calibrate on a small sample, then time a sample sized for ~target_seconds."""
-    A_host = host_csr(dA)
-    B64 = B.float().cpu().numpy().astype(np.float64)
-    perm = dv.row_perm64.cpu().numpy()
-    rp, bp, bc = dv.host_structure()
-    gw = group_widths(bounds, rp, bp, bc)
-    N = B64.shape[1]
-    s = cpu_sample(A_host, bounds, perm, rp, gw, N, 2e9)
-    t = time_cpu(s, bounds, B64, threads)
-    target = min(2e9 / max(t, 1e-6) * target_seconds, 1e15)
-    s = cpu_sample(A_host, bounds, perm, rp, gw, N, target)
-    t = time_cpu(s, bounds, B64, threads)
-    useful = 2.0 * s["nnz"] * N
-    return {"value": useful / t / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "seconds": t, "host": host_info(),
-            "sample": f"oracle.spmm_vbr_np (numpy port of multiply.py:72-97, float64, per-block dgemm, "
-                      f"threads={threads}) on the first {s['rows']} permuted rows ({s['block_rows']} block rows, "
-                      f"{s['nnz']} nnz) of the same VBR structure and B"}
+def cpu_baseline(args, target_seconds, threads):
+    """The reference CPU path (oracle structure + numpy spmm_vbr) on a bounded sample of the same
+    workload: consecutive chunks (1/64 of the VBR work each) until ~target_seconds have been spent."""
+    n_chunks = 64
+    w = reference_workload(args.config, args.scale, n_chunks)
+    C = np.zeros((w["n_rows"], w["N"]))
+    spent, flops, done = 0.0, 0.0, 0
+    while done < n_chunks and spent < target_seconds:
+        t, f = time_chunk(w, done, threads, C)
+        spent, flops, done = spent + t, flops + f, done + 1
+    rows = w["chunks"][done - 1][1]
+    return {"value": flops / spent / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "seconds": round(spent, 3), "host": host_info(), "setup": w["setup"],
+            "sample": f"reference path restated in oracle/ (C 1-SA + VBR build, numpy spmm_vbr of multiply.py:72-97, "
+                      f"float64 per-block dgemm, threads={threads}): the first {done} of {n_chunks} equal-work chunks "
+                      f"(block rows 0..{rows} of {w['n_groups']}) of the same matrix and B"}
 
 
 # ---------------------------------------------------------------------------------------- main
@@ -347,10 +348,7 @@ def run_ours(args, world, rank):
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
-        "config": {"workload": f"config {cfg.name}: {cfg.description}", "n_rows": dA.n_rows, "n_cols": dA.n_cols,
-                   "nnz": dA.nnz, "N": N, "delta": cfg.delta, "tau": cfg.tau, "policy": "jaccard, bounded, update",
-                   "parallelism": f"block-row shards x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed between steps (256 MiB memset outside the timed events)"},
+        "config": workload_config(cfg, dA.n_rows, dA.n_cols, dA.nnz, world),
         "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
         "csr_comparator": csr,
         "clocks": sampler.summary(),
@@ -359,7 +357,7 @@ def run_ours(args, world, rank):
                        padding_vbr_over_useful=round(info["vbr_flops"] * world / useful, 3)),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(dA, bounds, dv, B, args.cpu_seconds, os.cpu_count() or 1)
+        out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -432,50 +430,48 @@ class _ShardView:
 
 
 def run_reference(args, world, rank):
-    """The reference's CPU implementation of the path (numpy port, oracle/) on the host cores."""
+    """The reference's CPU implementation of the path on the host cores: oracle/ restatements only
+    (C 1-SA and VBR build, numpy spmm_vbr), never librowblock_b200.so.  The K timed steps multiply K
+    disjoint chunks of block rows (equal VBR work), so together they compute the whole product once."""
     if rank != 0:
         return
-    from paper_2202_05868_b200 import synth
-
-    cuda = torch.cuda.is_available()
-    device = torch.device("cuda", torch.cuda.current_device()) if cuda else torch.device("cpu")
-    if cuda:
-        dA, bounds, cfg, meta, dv, stages = build_workload(args, device)
-        perm = dv.row_perm64.cpu().numpy()
-        rp, bp, bc = dv.host_structure()
-    else:  # structure from the oracle's 1-SA when no GPU is present
-        import oracle
-
-        dA, bounds, cfg, meta = synth.make(args.config, scale=args.scale, device="cpu")
-        s = oracle.block_1sa_arrays(dA.row_ptr.numpy(), dA.col_idx.numpy(), bounds, tau=cfg.tau)
-        perm, rp = s["row_perm"], s["group_ptr"]
-        bp, bc = oracle.vbr_blocks(dA.row_ptr.numpy(), dA.col_idx.numpy(), bounds, perm, rp)
-    gw = group_widths(bounds, rp, bp, bc)
-    B = synth.make_b(cfg, dA.n_cols, cfg.precision, device="cpu")
-    B64 = B.float().numpy().astype(np.float64)
     threads = os.cpu_count() or 1
-    A_host = host_csr(dA)
-    per_step = min(2.0, 150.0 / max(1, args.steps + args.warmup))
-    N = B64.shape[1]
-    cal = cpu_sample(A_host, bounds, perm, rp, gw, N, 2e9)
-    t = time_cpu(cal, bounds, B64, threads)
-    sample = cpu_sample(A_host, bounds, perm, rp, gw, N, 2e9 / max(t, 1e-6) * per_step)
-    for _ in range(args.warmup):
-        time_cpu(sample, bounds, B64, threads)
-    times = [time_cpu(sample, bounds, B64, threads) for _ in range(args.steps)]
-    ms = 1e3 * float(np.mean(times))
-    value = 2.0 * sample["nnz"] * B64.shape[1] / (ms * 1e-3) / 1e9
-    desc = (f"oracle.spmm_vbr_np (numpy port of multiply.py:72-97, float64 per-block dgemm, threads={threads}) "
-            f"on the first {sample['rows']} permuted rows ({sample['nnz']} nnz) per step")
+    n_chunks = max(1, args.steps)
+    w = reference_workload(args.config, args.scale, n_chunks)
+    cfg = w["cfg"]
+    C = np.zeros((w["n_rows"], w["N"]))
+    for k in range(args.warmup):
+        time_chunk(w, k % n_chunks, threads, C)
+    C[:] = 0.0
+    times, flops = [], 0.0
+    for k in range(args.steps):
+        t, f = time_chunk(w, k, threads, C)
+        times.append(t)
+        flops += f
+    total = float(np.sum(times))
+    ms = 1e3 * total / args.steps
+    value = flops / total / 1e9
+    desc = (f"reference path restated in oracle/ (C 1-SA + VBR build, numpy spmm_vbr of multiply.py:72-97, "
+            f"float64 per-block dgemm, threads={threads}); the {args.steps} timed steps multiply {n_chunks} disjoint "
+            f"equal-work chunks of block rows, i.e. the whole product once")
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"config {cfg.name}: {cfg.description}", "n_rows": dA.n_rows, "n_cols": dA.n_cols,
-                      "nnz": dA.nnz, "N": cfg.N, "delta": cfg.delta, "tau": cfg.tau},
+           "config": workload_config(cfg, w["n_rows"], w["n_cols"], w["nnz"], world),
            "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
                             "sample": desc, "host": host_info()},
-           "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "stages": dict(w["setup"], n_groups=w["n_groups"], n_blocks=w["n_blocks"],
+                          product_checksum=float(C.sum()))}
     print(json.dumps(out), flush=True)
+
+
+def workload_config(cfg, n_rows, n_cols, nnz, world):
+    """The `config` dict, identical in both arms."""
+    return {"workload": f"config {cfg.name}: {cfg.description}", "n_rows": n_rows, "n_cols": n_cols, "nnz": nnz,
+            "N": cfg.N, "delta": cfg.delta, "tau": cfg.tau, "policy": "jaccard, bounded, update",
+            "parallelism": f"block-row shards x{world}" if world > 1 else "single GPU",
+            "l2": "flushed between steps (256 MiB memset outside the timed events)"}
 
 
 def main():

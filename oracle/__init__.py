@@ -14,6 +14,7 @@ Contents
 --------
 * ``block_1sa_arrays`` / ``quotient`` / ``vbr_blocks``: ctypes bindings to
   ``rowblock_oracle.c`` (C restatement of blocking.py:118-306, vbr.py:88-125).
+* ``vbr_payloads``: the float64 block payloads (``orc_vbr_scatter``, vbr.py:113-123).
 * ``spmm_vbr_np`` / ``spmm_csr_np``: numpy restatements of multiply.py:51-97
   (float64, per-block dgemm, the same ThreadPool chunking over block rows).
 """
@@ -51,6 +52,7 @@ def _load():
         lib.orc_block_1sa.argtypes = [I, P, P, P, I, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, P]
         lib.orc_vbr_blocks.argtypes = [I, P, P, P, I, P, P, I, P, P]
+        lib.orc_vbr_scatter.argtypes = [I, P, P, P, P, P, P, I, P, P, P, P]
         lib.orc_block_1sa_pruned.argtypes = [I, P, P, P, I, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, P, P]
         _lib = lib
@@ -146,38 +148,29 @@ def _chunks(n: int, parts: int):
 
 
 def vbr_payloads(row_ptr, col_idx, values, boundaries, row_perm, row_partition, blk_ptr, blk_col):
-    """Dense float64 payload per stored block (vbr.py:113-123), as a vectorised numpy scatter.
+    """Dense float64 payload per stored block (vbr.py:113-123), scattered by ``orc_vbr_scatter``.
 
-    Returns a list (per block row g) of lists of (bcol, payload[h_g, w_bcol]) with bcols ascending.
+    Returns a list (per block row g) of lists of (bcol, payload[h_g, w_bcol]) with bcols ascending;
+    every payload is a view into one flat float64 buffer.
     """
     row_ptr, col_idx, b = _c64(row_ptr), _c64(col_idx), _c64(boundaries)
-    values = np.asarray(values, dtype=np.float64)
+    values = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
     rp, bp, bc = _c64(row_partition), _c64(blk_ptr), _c64(blk_col)
+    perm = _c64(row_perm)
     n = len(row_ptr) - 1
     H = len(rp) - 1
-    n_seg = len(b) - 1
     widths = np.diff(b)
     heights = np.diff(rp)
-    blk_g = np.repeat(np.arange(H), np.diff(bp))
-    blk_h = heights[blk_g]
+    blk_h = np.repeat(heights, np.diff(bp))
     blk_w = widths[bc] if len(bc) else np.zeros(0, np.int64)
     blk_off = np.zeros(len(bc) + 1, np.int64)
     np.cumsum(blk_h * blk_w, out=blk_off[1:])
-    flat = np.zeros(int(blk_off[-1]), np.float64)
+    flat = np.zeros(max(int(blk_off[-1]), 1), np.float64)
     if len(col_idx):
-        pos = np.empty(n, np.int64)
-        pos[_c64(row_perm)] = np.arange(n)
-        grp_of_pos = np.repeat(np.arange(H), heights)
-        rows = np.repeat(np.arange(n), np.diff(row_ptr))
-        p = pos[rows]
-        g = grp_of_pos[p]
-        local = p - rp[g]
-        seg = np.searchsorted(b, col_idx, side="right") - 1
-        gkey = blk_g * (n_seg + 1) + bc
-        blk = np.searchsorted(gkey, g * (n_seg + 1) + seg)
-        if np.any(blk >= len(bc)) or np.any(gkey[np.minimum(blk, len(bc) - 1)] != g * (n_seg + 1) + seg):
-            raise ValueError("nonzero outside the stored blocks")
-        flat[blk_off[blk] + local * blk_w[blk] + (col_idx - b[seg])] = values
+        rc = _load().orc_vbr_scatter(n, _ptr(row_ptr), _ptr(col_idx), _ptr(values), _ptr(b), _ptr(perm), _ptr(rp), H,
+                                     _ptr(bp), _ptr(bc), _ptr(blk_off), _ptr(flat))
+        if rc != 0:
+            raise ValueError("nonzero outside the stored blocks" if rc == -3 else "oracle: bad row_perm")
     out = []
     for gg in range(H):
         out.append([(int(bc[k]), flat[blk_off[k]:blk_off[k + 1]].reshape(int(blk_h[k]), int(blk_w[k])))
@@ -186,12 +179,13 @@ def vbr_payloads(row_ptr, col_idx, values, boundaries, row_perm, row_partition, 
 
 
 def spmm_vbr_np(payloads, row_perm, row_partition, boundaries, B: np.ndarray, threads: int = 1,
-                block_rows=None) -> np.ndarray:
+                block_rows=None, out=None) -> np.ndarray:
     """multiply.py:72-97: per block row, acc = sum over blocks (ascending bcol) of payload @ B panel,
-    then C[row_perm[lo:hi]] = acc.  Empty block rows are skipped (their C rows stay exactly 0)."""
+    then C[row_perm[lo:hi]] = acc.  Empty block rows are skipped (their C rows stay exactly 0).
+    ``block_rows`` restricts the product to those block rows; ``out`` receives their C rows."""
     n_rows = len(row_perm)
     B = np.asarray(B, dtype=np.float64)
-    C = np.zeros((n_rows, B.shape[1]))
+    C = np.zeros((n_rows, B.shape[1])) if out is None else out
     b = _c64(boundaries)
     rp = _c64(row_partition)
     perm = _c64(row_perm)

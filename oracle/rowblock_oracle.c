@@ -18,6 +18,8 @@
  *                     _greedy_merge 209-266 in its scalar form (merge_condition 184-203),
  *                     _build_grouping 269-280
  *   orc_vbr_blocks    vbr.py:88-125 (stored block columns per block row, recomputed from data)
+ *   orc_vbr_scatter   vbr.py:113-123 (float64 payload of every stored block)
+ *   orc_block_1sa_pruned  the same greedy scan with exact candidate pruning (config 3 sizes)
  */
 #include <math.h>
 #include <stdint.h>
@@ -440,5 +442,31 @@ int orc_block_1sa_pruned(int64_t n_rows, const int64_t* row_ptr, const int64_t* 
   free(mark); free(mem_ptr); free(mem); free(icnt); free(cnt); free(iptr); free(gcur);
   free(P); free(plist); free(order); free(group_of_item); free(seed_item); free(stamp); free(okv); free(cand); free(empt);
   free(isz); free(post_ptr); free(post); free(fill); free(rs_ptr); free(rs); free(item_of_row); free(reps);
+  return 0;
+}
+
+/* Dense float64 payloads of the stored blocks (vbr.py:113-123): block k of block row g is an
+ * h_g x w_{bcol} row-major array at flat[blk_off[k]], zero except the nonzeros of g's rows,
+ * scattered at [local row, col - bounds[bcol]].  Blocks of a row are ascending in bcol and a row's
+ * columns are ascending, so one forward walk over the row's blocks places every nonzero.
+ * Returns 0, or -3 if a nonzero lies outside the row's stored blocks.                          */
+int orc_vbr_scatter(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                    const int64_t* bounds, const int64_t* row_perm, const int64_t* row_partition, int64_t H,
+                    const int64_t* blk_ptr, const int64_t* blk_col, const int64_t* blk_off, double* flat) {
+  for (int64_t g = 0; g < H; ++g) {
+    const int64_t b0 = blk_ptr[g], b1 = blk_ptr[g + 1];
+    for (int64_t p = row_partition[g]; p < row_partition[g + 1]; ++p) {
+      const int64_t r = row_perm[p], local = p - row_partition[g];
+      if (r < 0 || r >= n_rows) return -2;
+      int64_t k = b0;
+      for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) {
+        const int64_t c = col_idx[q];
+        while (k < b1 && bounds[blk_col[k] + 1] <= c) ++k;
+        if (k == b1 || bounds[blk_col[k]] > c) return -3;
+        const int64_t w = bounds[blk_col[k] + 1] - bounds[blk_col[k]];
+        flat[blk_off[k] + local * w + (c - bounds[blk_col[k]])] = values[q];
+      }
+    }
+  }
   return 0;
 }

@@ -171,6 +171,51 @@ def make(name: str, scale: int = 1, device=None, precision: str | None = None):
     return A, bounds, cfg, meta
 
 
+def _blocked_host(rng, n: int, d: int, theta: float, prec: str):
+    """Config 5's matrix (planted d x d blocks, rho = 1, no noise, rows scrambled) built straight in
+    CSR order with numpy: identical arrays to ``make('5')`` (same draws in the same order) without
+    sorting 687M keys.  Output row i is input row perm[i]; its columns are the 64 columns of every
+    selected block of block row perm[i] // d, ascending."""
+    bc = n // d
+    n_sel = _round_half_up(theta * bc * bc)
+    blocks = np.sort(rng.choice(bc * bc, size=n_sel, replace=False))
+    perm_r = rng.permutation(n)
+    b_row, b_col = blocks // bc, blocks % bc
+    nblk = np.bincount(b_row, minlength=bc).astype(np.int64)
+    start = np.zeros(bc + 1, np.int64)
+    np.cumsum(nblk, out=start[1:])
+    br = perm_r // d                       # input block row of every output row
+    k = nblk[br]
+    row_ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(k * d, out=row_ptr[1:])
+    kp = np.zeros(n + 1, np.int64)
+    np.cumsum(k, out=kp[1:])
+    ent = np.repeat(start[br] - kp[:-1], k) + np.arange(int(kp[-1]), dtype=np.int64)
+    col_idx = (b_col[ent][:, None] * d + np.arange(d, dtype=np.int64)[None, :]).reshape(-1)
+    values = _values(rng, int(row_ptr[-1]), prec)
+    return row_ptr, col_idx, values, n_sel * d * d
+
+
+def make_host(name: str, scale: int = 1, precision: str | None = None):
+    """Config ``name`` as host numpy CSR arrays -> (row_ptr, col_idx, values float64, boundaries, Config).
+
+    Same matrix as ``make`` (bit-identical arrays); config 5 takes a sort-free numpy path, the others
+    run ``make`` on the CPU.  Used by the CPU reference arm, which must not touch the GPU library."""
+    cfg = CONFIGS[name]
+    prec = precision or cfg.precision
+    if name == "5":
+        rng = np.random.default_rng(SEEDS[name])
+        n = cfg.n_rows // scale
+        row_ptr, col_idx, values, _ = _blocked_host(rng, n, 64, 0.01, prec)
+        n_cols = n
+    else:
+        A, _, _, _ = make(name, scale=scale, device="cpu", precision=prec)
+        row_ptr, col_idx, values = A.row_ptr.numpy(), A.col_idx.numpy(), A.values.numpy()
+        n_cols = A.n_cols
+    bounds = np.append(np.arange(0, n_cols, cfg.delta, dtype=np.int64), n_cols)
+    return row_ptr, col_idx, values, bounds, cfg
+
+
 def make_b(cfg: Config, n_cols: int, precision: str, device=None, seed: int = 1234) -> torch.Tensor:
     """B = U[0,1) rounded to the kernel dtype, [n_cols, N] row-major, on the device."""
     dev = _dev(device)
