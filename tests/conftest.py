@@ -39,7 +39,7 @@ def golden_b(case):
     return None
 
 
-MEDIUM = ["cfg1_full", "cfg2b_s16", "cfg4_s8", "cfg5_s32", "rmat12_t3", "rmat12_t9"]
+MEDIUM = ["cfg1_full", "cfg2b_s16", "cfg4_s8", "cfg5_s32", "rmat12_t3", "rmat12_t9", "rmat16_t7"]
 
 
 @pytest.fixture(scope="session")

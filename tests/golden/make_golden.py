@@ -148,6 +148,24 @@ def nonuniform_cases():
     return cases
 
 
+def rmat_cases():
+    """Config 3 flavour (R-MAT, rows scrambled, Δ=32) with B, so the skinny SpMM path is checked
+    against spmm_vbr (multiply.py:72-97) on power-law input: 2^12 at τ ∈ {0.3, 0.9} (N=64) and
+    2^16 at τ=0.7 (N=128, config 3's N; C checksums only)."""
+    cases = []
+    R = rb.gen_rmat(rb.RmatSpec(12, 16, seed=3))
+    Rs, _ = rb.scramble(R, 33)
+    for tau in (0.3, 0.9):
+        cases.append(record(f"rmat12_t{int(tau * 10)}", Rs, rb.ColumnPartition.uniform(R.n_cols, 32),
+                            rb.MergePolicy(tau=tau), True, B=np.random.default_rng(34).random((R.n_cols, 64)),
+                            store_c=False, b_seed=34))
+    R = rb.gen_rmat(rb.RmatSpec(16, 16, seed=3))
+    Rs, _ = rb.scramble(R, 36)
+    cases.append(record("rmat16_t7", Rs, rb.ColumnPartition.uniform(R.n_cols, 32), rb.MergePolicy(tau=0.7), True,
+                        B=np.random.default_rng(37).random((R.n_cols, 128)), store_c=False, b_seed=37))
+    return cases
+
+
 def medium_cases():
     """Scaled versions of the BASELINE configs (structure + C checksums)."""
     cases = []
@@ -168,12 +186,7 @@ def medium_cases():
     A = random_csr(rng, 512, 4096, 0.1)
     cases.append(record("cfg4_s8", A, rb.ColumnPartition.uniform(4096, 128), rb.MergePolicy(tau=0.7), True,
                         B=np.random.default_rng(45).random((4096, 128)), store_c=False, b_seed=45))
-    # R-MAT 2^12 scrambled, Δ=32, τ ∈ {0.3, 0.9}
-    R = rb.gen_rmat(rb.RmatSpec(12, 16, seed=3))
-    Rs, _ = rb.scramble(R, 33)
-    for tau in (0.3, 0.9):
-        cases.append(record(f"rmat12_t{int(tau * 10)}", Rs, rb.ColumnPartition.uniform(R.n_cols, 32),
-                            rb.MergePolicy(tau=tau), True))
+    cases += rmat_cases()
     # hidden blocks + noise, rows scrambled only (config 2b flavour) at 2048^2
     A = rb.gen_blocked(rb.BlockedMatrixSpec(2048, 2048, 64, 0.05, 1.0, seed=2))
     S, _ = rb.scramble(A, 22)
@@ -182,6 +195,11 @@ def medium_cases():
 
 
 def main():
+    if "--rmat" in sys.argv:  # regenerate only the R-MAT cases
+        for n, d in rmat_cases():
+            np.savez_compressed(os.path.join(OUT, f"golden_{n}.npz"), **{k: np.asarray(v) for k, v in d.items()})
+            print("wrote", n)
+        return
     allc = kat_cases() + random_cases() + nonuniform_cases() + medium_cases()
     small = {n: d for n, d in allc if not n.startswith(("cfg", "rmat"))}
     np.savez_compressed(os.path.join(OUT, "golden_small.npz"),

@@ -4,6 +4,8 @@ run this size; the oracle takes ~8 min per τ on one core, so th
 SHA-256 digest of each output array plus the input's digest (synth is deterministic across machines).
 
     python tests/golden/make_golden_cfg3.py 0.9,0.7
+
+RB_GOLDEN_OUT=<file> writes elsewhere (to run several τ in parallel and merge the entries).
 """
 import hashlib
 import json
@@ -17,7 +19,7 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 from paper_2202_05868_b200 import synth  # noqa: E402
 
-OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_cfg3_full.json")
+OUT = os.environ.get("RB_GOLDEN_OUT") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_cfg3_full.json")
 
 
 def digest(a) -> str:

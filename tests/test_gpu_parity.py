@@ -146,9 +146,14 @@ def test_spmm_golden_small(golden_small, precision):
     assert n_checked > 100
 
 
-@pytest.mark.parametrize("name", ["cfg1_full", "cfg4_s8", "cfg5_s32"])
+@pytest.mark.parametrize("name", ["cfg1_full", "cfg4_s8", "cfg5_s32", "rmat12_t3", "rmat12_t9", "rmat16_t7"])
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_spmm_medium_checksums(name, precision):
+    """C of the reference's spmm_vbr (multiply.py:72-97) pinned by two checksums per row (C·r and
+    the row sums) recorded when the golden case was made; the R-MAT cases run the skinny kernels
+    on power-law input (config 3's shape)."""
+    import scipy.sparse as sp
+
     case = load_golden(name)
     B = golden_b(case)
     A, q = csr_of(case), part_of(case)
@@ -156,9 +161,12 @@ def test_spmm_medium_checksums(name, precision):
     C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision=precision).data
     r = np.random.default_rng(7).standard_normal(B.shape[1])
     tol = 1e-5 if precision == "fp32" else 1e-2
-    scale = (np.abs(A.to_dense()) @ np.abs(B)) @ np.abs(r)
-    assert np.all(np.abs(C @ r - case["C_dot_r"]) <= tol * scale + 1e-12)
-    assert np.all(np.abs(C.sum(axis=1) - case["C_rowsum"]) <= tol * (np.abs(A.to_dense()) @ np.abs(B)).sum(1) + 1e-12)
+    Aabs = sp.csr_matrix((np.abs(A.values), A.col_idx, A.row_ptr), shape=(A.n_rows, A.n_cols))
+    AB = Aabs @ np.abs(B)
+    assert np.all(np.abs(C @ r - case["C_dot_r"]) <= tol * (AB @ np.abs(r)) + 1e-12)
+    assert np.all(np.abs(C.sum(axis=1) - case["C_rowsum"]) <= tol * AB.sum(1) + 1e-12)
+    empty = np.diff(A.row_ptr) == 0
+    assert np.all(C[empty] == 0.0)
 
 
 def test_spmm_tall_and_short_shapes_bf16():
