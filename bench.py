@@ -320,7 +320,8 @@ def run_ours(args, world, rank):
     exec_tflops = info["executed_flops"] / (ms_local * 1e-3) / 1e12
     tensor_dominant = prec != "fp32" and info["core_vbr_flops"] < 0.5 * info["vbr_flops"]
     if tensor_dominant:
-        roof = {"bound": "tensor", "kernel": "spmm_tall2_kernel" if info["n_items_tall"] else "spmm_short2_kernel",
+        roof = {"bound": "tensor", "kernel": ("spmm_tall2_kernel" if info["n_items_tall"] else
+                                               "spmm_sweep_kernel" if info["n_sweep_steps"] else "spmm_short2_kernel"),
                 "achieved": round(achieved_tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(achieved_tflops / peaks["bf16_tflops"], 5), "traffic": profile_traffic(args.config),
                 "peak_source": peaks["source"] + " (burst bf16, kernel timed alone)",

@@ -140,7 +140,7 @@ typedef struct rb_spmm_plan rb_spmm_plan;
 
 typedef struct rb_spmm_info {
   int64_t n_items_tall;      /* (block row, 128-row M-tile, 256-col N-chunk) work items */
-  int64_t n_items_short;     /* (block row, 256-col N-chunk) swap-AB work items */
+  int64_t n_items_short;     /* (block row, 256-col N-chunk) swap-AB work items (+ sweep steps) */
   int64_t n_items_simt;      /* fp32 check-path work items */
   double executed_flops;     /* 2 * sum over tiles of hp * dp * N_pad (MMA-padded work) */
   double vbr_flops;          /* 2 * stored_area * N (VBR-padded work) */
@@ -148,6 +148,8 @@ typedef struct rb_spmm_info {
   int64_t n_items_skinny;    /* (block row, C-column slab) CUDA-core items for block rows with h <= 8 */
   int64_t n_launches;        /* kernel launches per rb_spmm_execute */
   double core_vbr_flops;     /* part of vbr_flops run on the CUDA cores (skinny / fp32 kernels) */
+  int64_t n_sweep_steps;     /* block steps of the multi-slot sweep kernel (0: not used) */
+  int64_t sweep_slots;       /* block rows resident in TMEM per CTA on the sweep kernel */
 } rb_spmm_info;
 
 int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t b_dtype, int32_t shard,

@@ -49,7 +49,8 @@ class Sparse24Device(ctypes.Structure):
 class SpmmInfo(ctypes.Structure):
     _fields_ = [("n_items_tall", I64), ("n_items_short", I64), ("n_items_simt", I64),
                 ("executed_flops", ctypes.c_double), ("vbr_flops", ctypes.c_double), ("row_begin_perm", I64),
-                ("n_items_skinny", I64), ("n_launches", I64), ("core_vbr_flops", ctypes.c_double)]
+                ("n_items_skinny", I64), ("n_launches", I64), ("core_vbr_flops", ctypes.c_double),
+                ("n_sweep_steps", I64), ("sweep_slots", I64)]
 
 
 _lib = None

@@ -755,6 +755,286 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// short block rows of one height class on a static multi-slot sweep (swap-AB, one CTA).
+//
+// Config 5 (4,096 block rows of h = 64, each ~41 blocks spread uniformly over 4,096 block columns,
+// N = 1024) has no B reuse inside a CTA: every B panel an SM fetches is used by one block row.
+// Reuse can only come from L2, across the block rows that are resident on the chip at the same
+// time.  Round 1 ran one (block row, 256-column slab) item per CTA at a time, each sweeping its
+// blocks from block column 0: 148 rows in flight at random phases, so the L2 working set was the
+// whole 134 MB slab of B (> the ~90 MB hot L2) and 48 % of the B panel bytes came from DRAM.
+// Here each CTA keeps `n_slots` block rows resident in TMEM (slot s = columns s*2*hp .. +2*hp: two
+// M-tiles of 128 C columns x hp rows; 4 slots at hp = 64 fill the 512 columns) and walks a
+// plan-time step list that merges the slots' blocks in CIRCULAR block-column order: a block row
+// that enters a freed slot starts at the CTA's current block column and wraps around.  All CTAs
+// therefore sweep B in near lockstep with 4x more rows in flight, the live B window is a small
+// arc of the slab, and every B panel fetched from DRAM serves ~6 block rows (tools/l2sim.py,
+// calibrated on the round-1 schedule: 16.0 -> 10.6 GB of A + B misses per step).
+// The per-row accumulation order is fixed by the plan (rotated ascending block columns), so C is
+// run-to-run deterministic.  Slot handshakes: the MMA thread commits sdone[s] after a row's last
+// block; the epilogue drains slot s and the 4 epilogue warps arrive on sfree[s]; the MMA waits on
+// sfree[s] before the first block of the next row in slot s (the plan leaves `delay` steps of
+// other slots' work between the two so the drain overlaps MMAs).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}" : "=r"(pred));
+  return pred != 0;
+}
+
+constexpr int MAX_SLOTS = 16;
+constexpr uint32_t SMEM_SWEEP = S_STAGES * S_STAGE + 1024 + 512;
+
+struct SweepArgs {
+  const int4* steps;        // (A tile row, first B row, n0, slot | first << 8 | last << 9)
+  const int32_t* step_ptr;  // CTA b's steps are [step_ptr[b], step_ptr[b+1])
+  const int4* done;         // row completions in commit order: (g, n0, slot, -)
+  const int32_t* done_ptr;
+  int32_t hp;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    spmm_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SpmmArgs a,
+                      SweepArgs w) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_STAGES * S_STAGE);
+  uint64_t* empty = full + S_STAGES;
+  uint64_t* sdone = empty + S_STAGES;
+  uint64_t* sfree = sdone + MAX_SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + MAX_SLOTS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hp = w.hp;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < MAX_SLOTS; ++s) {
+      mbar_init(&sdone[s], 1);
+      mbar_init(&sfree[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int s_begin = w.step_ptr[blockIdx.x], s_end = w.step_ptr[blockIdx.x + 1];
+
+  // Producer and MMA warps run converged: per-step values are loaded by every lane (the next step's
+  // ahead of time), broadcast with __shfl_sync so the compiler keeps them warp-uniform, and one
+  // elected lane issues the TMA / tcgen05 instructions.  (A lone lane-0 loop made ptxas wrap every
+  // UTCHMMA in an ELECT / R2UR.BROADCAST waterfall and left a dependent global load in front of
+  // each step: ~165 cycles per M=128 N=64 MMA against the 48-cycle issue floor measured by
+  // tools/mma_probe.)
+  if (warp == 0) {
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmA);
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    PipeState ps;
+    int4 nxt = s_begin < s_end ? w.steps[s_begin] : make_int4(0, 0, 0, 0);
+    for (int i = s_begin; i < s_end; ++i) {
+      int4 st = nxt;
+      if (i + 1 < s_end) nxt = w.steps[i + 1];
+      const int row0 = __shfl_sync(0xffffffffu, st.x, 0), krow0 = __shfl_sync(0xffffffffu, st.y, 0);
+      const int n0 = __shfl_sync(0xffffffffu, st.z, 0);
+      const int n_boxes = min(a.short_ns / 64, (a.N - n0 + 63) / 64);
+      const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
+      for (int kc = 0; kc < a.dp_chunks; ++kc) {
+        if (elect_one()) {
+          mbar_wait(&empty[ps.s], ps.ph ^ 1);
+#ifdef RB_DBG_NOLOAD  // developer experiment: MMA + barrier pipeline without any operand traffic
+          mbar_arrive(&full[ps.s]);
+#else
+          mbar_arrive_expect_tx(&full[ps.s], tx);
+          uint8_t* sA = smem + ps.s * S_STAGE;
+          uint8_t* sB = sA + S_A_SLOT;
+          tma_load_2d_hint(sA, &tmA, &full[ps.s], kc * KCH, row0, pol_a);
+          for (int bx = 0; bx < n_boxes; ++bx)
+            tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[ps.s], n0 + 64 * bx, krow0 + kc * KCH, pol_b);
+#endif
+        }
+        __syncwarp();
+        ps.advance(S_STAGES);
+      }
+    }
+    for (int k = 0; k < S_STAGES; ++k) {
+      mbar_wait(&empty[ps.s], ps.ph ^ 1);
+      ps.advance(S_STAGES);
+    }
+  } else if (warp == 1) {
+    PipeState ps;
+#ifdef RB_PROF_SWEEP
+    long long prof_free = 0, prof_full = 0;
+    const long long prof_t0 = clock64();
+#endif
+    uint32_t use_ph = 0;  // bit s: parity of slot s's next sfree wait (flipped per row)
+    const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
+    const uint64_t adesc0 = sdesc_sw128(smem_u32(smem) + S_A_SLOT, BOX_BYTES, 1024);  // B panel (MN-major)
+    const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem), 16, 1024);                    // tile rows (K-major)
+    int4 nxt = s_begin < s_end ? w.steps[s_begin] : make_int4(0, 0, 0, 0);
+    for (int i = s_begin; i < s_end; ++i) {
+      int4 st = nxt;
+      if (i + 1 < s_end) nxt = w.steps[i + 1];
+      const int n0 = __shfl_sync(0xffffffffu, st.z, 0), fl = __shfl_sync(0xffffffffu, st.w, 0);
+      const int slot = fl & 0xff;
+      const bool first = (fl >> 8) & 1, last = (fl >> 9) & 1;
+      const int n_mt = min(a.short_ns / 128, (a.N - n0 + 127) / 128);
+      if (first) {
+#ifdef RB_PROF_SWEEP
+        const long long t0 = clock64();
+#endif
+        mbar_wait(&sfree[slot], ((use_ph >> slot) & 1) ^ 1);
+#ifdef RB_PROF_SWEEP
+        prof_free += clock64() - t0;
+#endif
+        use_ph ^= 1u << slot;
+        tc_fence_after();
+      }
+      const uint32_t d = tmem + (uint32_t)(slot * 2 * hp);
+      for (int kc = 0; kc < a.dp_chunks; ++kc) {
+        // descriptors = stage-0 descriptor + (byte offset >> 4): one add per operand (SMEM < 256 KB,
+        // so the 14-bit address field never carries)
+        const uint64_t soff = (uint64_t)((ps.s * S_STAGE) >> 4);
+        if (elect_one()) {  // one lane waits and issues (a SYNCS wait by the whole warp costs more)
+#ifdef RB_PROF_SWEEP
+          const long long t1 = clock64();
+#endif
+          mbar_wait(&full[ps.s], ps.ph);
+#ifdef RB_PROF_SWEEP
+          prof_full += clock64() - t1;
+#endif
+          tc_fence_after();
+          if (n_mt == 2) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int kk = 0; kk < KCH / 16; ++kk)
+                umma_f16(d + mt * hp, adesc0 + soff + ((mt * 2 * BOX_BYTES + kk * 2048) >> 4), bdesc0 + soff + kk * 2,
+                         idesc, !(first && kc == 0 && kk == 0));
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < KCH / 16; ++kk)
+              umma_f16(d, adesc0 + soff + ((kk * 2048) >> 4), bdesc0 + soff + kk * 2, idesc,
+                       !(first && kc == 0 && kk == 0));
+          }
+          umma_commit(&empty[ps.s]);
+          if (last && kc + 1 == a.dp_chunks) umma_commit(&sdone[slot]);
+        }
+        __syncwarp();
+        ps.advance(S_STAGES);
+      }
+    }
+#ifdef RB_PROF_SWEEP
+    if (blockIdx.x % 37 == 0 && lane == 0)
+      printf("sweep cta %d mma: total %lld wait_free %lld wait_full %lld steps %d\n", blockIdx.x, clock64() - prof_t0,
+             prof_free, prof_full, s_end - s_begin);
+#endif
+  } else {
+    // epilogue: drain finished slots in commit order; TMEM lane = C column, a warp stores 32
+    // consecutive floats (128 B) of one C row per instruction
+    const int q = warp & 3;
+    uint32_t done_ph = 0;
+#ifdef RB_PROF_SWEEP
+    long long prof_wait = 0, prof_drain = 0, prof_max = 0, prof_ld = 0;
+#endif
+    for (int j = w.done_ptr[blockIdx.x]; j < w.done_ptr[blockIdx.x + 1]; ++j) {
+      const int4 c = w.done[j];
+      const int g = c.x, n0 = c.y, slot = c.z;
+      const int p0 = a.row_partition[g];
+      const int h = a.row_partition[g + 1] - p0;
+      const int n_mt = min(a.short_ns / 128, (a.N - n0 + 127) / 128);
+#ifdef RB_PROF_SWEEP
+      const long long e0 = clock64();
+#endif
+      mbar_wait(&sdone[slot], (done_ph >> slot) & 1);
+#ifdef RB_PROF_SWEEP
+      const long long e1 = clock64();
+      prof_wait += e1 - e0;
+#endif
+      done_ph ^= 1u << slot;
+      tc_fence_after();
+      const uint32_t t0 = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(slot * 2 * hp);
+      // the row's C row indices, one per lane (two registers cover h <= 64), fetched once: a load
+      // per store would put 64 dependent global loads on the drain's critical path
+      const int rp_lo = lane < h ? a.row_perm[p0 + lane] : 0;
+      const int rp_hi = lane + 32 < h ? a.row_perm[p0 + 32 + lane] : 0;
+      if (hp <= 64) {
+        // Copy the whole slot (<= 2 M-tiles x 64 rows) to registers, hand the slot back to the MMA
+        // warp, then store: the slot's reuse waits only for the TMEM reads, not for the C stores.
+        uint32_t r[2][64];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          if (mt < n_mt) {
+            const uint32_t ta = t0 + (uint32_t)(mt * hp);
+            if (hp == 16) {
+              tmem_ld_32x32b_x16(ta, *reinterpret_cast<uint32_t(*)[16]>(r[mt]));
+            } else {
+              tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(r[mt]));
+              if (hp == 64) tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(r[mt] + 32));
+            }
+          }
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[slot]);
+#ifdef RB_PROF_SWEEP
+        prof_ld += clock64() - e1;
+#endif
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int n = n0 + mt * 128 + q * 32 + lane;
+          const bool nvalid = mt < n_mt && n < a.N;
+#pragma unroll
+          for (int jj = 0; jj < 64; ++jj) {
+            const int row = __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31);
+            if (nvalid && jj < h) a.C[(int64_t)row * a.ldc + n] = __uint_as_float(r[mt][jj]);
+          }
+        }
+      } else {
+        for (int mt = 0; mt < n_mt; ++mt) {
+          const int n = n0 + mt * 128 + q * 32 + lane;
+          const bool nvalid = n < a.N;
+          for (int j0 = 0; j0 < h; j0 += 64) {  // up to 64 rows per TMEM round trip
+            uint32_t r[64];
+            const uint32_t ta = t0 + (uint32_t)(mt * hp + j0);
+            tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(r));
+            tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 64; ++jj) {
+              const int row = j0 == 0 ? __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31)
+                                      : a.row_perm[p0 + j0 + jj];
+              if (nvalid && j0 + jj < h) a.C[(int64_t)row * a.ldc + n] = __uint_as_float(r[jj]);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[slot]);
+      }
+#ifdef RB_PROF_SWEEP
+      const long long e2 = clock64();
+      prof_drain += e2 - e1;
+      prof_max = max(prof_max, e2 - e1);
+#endif
+    }
+#ifdef RB_PROF_SWEEP
+    if (blockIdx.x % 37 == 0 && lane == 0)
+      printf("sweep cta %d epi warp %d: wait %lld drain %lld (tmem->regs %lld) max_drain %lld rows %d\n", blockIdx.x,
+             warp, prof_wait, prof_drain, prof_ld, prof_max, w.done_ptr[blockIdx.x + 1] - w.done_ptr[blockIdx.x]);
+#endif
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------
 // fp32 check path: CTA = (g, 8-row chunk r0, 128-col chunk n0); thread = one C column.
 // Per row the accumulation order is blocks ascending, then k ascending (fixed, deterministic).
 __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, const float* __restrict__ tiles,
@@ -939,6 +1219,13 @@ struct rb_spmm_plan {
   unsigned long long* d_sched = nullptr;  // 2 work counters per skinny height class
   int64_t skinny_off[rb::SKINNY_CLASSES + 1] = {0, 0, 0, 0, 0};
   CUtensorMap tmA16, tmA32, tmA64, tmA128;
+  // multi-slot sweep (spmm_sweep_kernel) for the dominant short height class
+  int4* d_sw_steps = nullptr;
+  int32_t* d_sw_step_ptr = nullptr;
+  int4* d_sw_done = nullptr;
+  int32_t* d_sw_done_ptr = nullptr;
+  int32_t sw_hp = 0, sw_ctas = 0, sw_slots = 0;
+  int64_t n_sw_steps = 0;
   rb_spmm_info info;
 };
 
@@ -1048,6 +1335,124 @@ static void short_schedule(std::vector<int4>& items, int ctas, int dpc, bool sla
   std::vector<int32_t> pos(cta_ptr.begin(), cta_ptr.end() - 1);
   for (size_t i = 0; i < items.size(); ++i) out[pos[owner[i]]++] = items[i];
   items.swap(out);
+}
+
+// Static multi-slot sweep schedule (spmm_sweep_kernel).  Block rows are assigned to CTAs by LPT on
+// their block counts (the same rows for every slab); CTA c's queue is its rows for slab 0, then for
+// slab 1, ...  A CTA holds n_slots rows at a time and repeatedly takes, among the resident rows
+// whose slot is usable, the one whose next block column is the nearest ahead of the CTA's current
+// block column (circular), so it sweeps block columns 0..nbc-1 over and over with all its rows
+// merged.  A row entering a slot starts at the first of its blocks at or after the current block
+// column (rotation) and wraps around.  A freed slot becomes usable `delay` steps after its row's
+// last step (time for the epilogue to drain it while the other slots keep the MMA busy).
+static void sweep_schedule(const std::vector<int32_t>& rows, const std::vector<int32_t>& slabs,
+                           const std::vector<int32_t>& rp, const std::vector<int32_t>& bp,
+                           const std::vector<int32_t>& bcol, const std::vector<int64_t>& tile_row,
+                           const std::vector<int32_t>& col_bounds, int64_t n_seg, int ctas, int n_slots, int delay,
+                           int dpc, std::vector<int4>& steps, std::vector<int32_t>& step_ptr, std::vector<int4>& done,
+                           std::vector<int32_t>& done_ptr) {
+  std::vector<std::vector<int32_t>> mine(ctas);
+  {
+    std::vector<int32_t> order(rows);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return bp[x + 1] - bp[x] > bp[y + 1] - bp[y]; });
+    using E = std::pair<double, int>;
+    std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
+    for (int c = 0; c < ctas; ++c) heap.push({0.0, c});
+    for (int32_t g : order) {
+      E top = heap.top();
+      heap.pop();
+      mine[top.second].push_back(g);
+      heap.push({top.first + (bp[g + 1] - bp[g]) * (double)dpc + 2.0, top.second});
+    }
+  }
+  steps.clear();
+  done.clear();
+  step_ptr.assign(1, 0);
+  done_ptr.assign(1, 0);
+  struct Slot {
+    int32_t g = -1, n0 = 0, nb = 0, start = 0, count = 0;
+    bool started = false;
+    int64_t usable = 0;
+    int32_t first_phase = -1;  // start column of the slot's first row (staggered); -1 afterwards
+  };
+  for (int c = 0; c < ctas; ++c) {
+    std::vector<int2> queue;  // (g, n0)
+    for (int32_t n0 : slabs)
+      for (int32_t g : mine[c]) queue.push_back(make_int2(g, n0));
+    size_t qi = 0;
+    // A row ends where it started (it wraps around once), so rows that start together also finish
+    // together and their drains would queue behind each other while the MMA waits for a slot.  The
+    // slots' first rows therefore start at evenly spaced block columns; every later row starts
+    // where its slot's previous row ended, so completions stay spread over the revolution.
+    std::vector<Slot> slot(n_slots);
+    for (int s = 0; s < n_slots; ++s) slot[s].first_phase = (int32_t)((int64_t)s * n_seg / n_slots);
+    int32_t phase = 0;
+    int64_t k = 0;
+    int active = 0;
+    for (;;) {
+      for (int s = 0; s < n_slots; ++s)
+        if (slot[s].g < 0 && qi < queue.size()) {
+          slot[s].g = queue[qi].x;
+          slot[s].n0 = queue[qi].y;
+          slot[s].nb = bp[slot[s].g + 1] - bp[slot[s].g];
+          slot[s].count = 0;
+          slot[s].started = false;
+          ++qi;
+          ++active;
+        }
+      if (active == 0) break;
+      int best = -1;
+      int64_t best_key = 0;
+      for (int s = 0; s < n_slots; ++s) {
+        Slot& r = slot[s];
+        if (r.g < 0) continue;
+        const int32_t* cols = bcol.data() + bp[r.g];
+        if (!r.started && r.usable <= k) {  // rotation: first block at or after the current column
+          const int32_t at = r.first_phase >= 0 ? r.first_phase : phase;
+          r.first_phase = -1;
+          r.start = (int32_t)(std::lower_bound(cols, cols + r.nb, at) - cols);
+          if (r.start == r.nb) r.start = 0;
+          r.started = true;
+        }
+        int64_t key;
+        if (!r.started) {
+          key = (int64_t)1 << 40 | r.usable;  // not usable yet: only if nothing else is
+        } else {
+          const int32_t b = cols[(r.start + r.count) % r.nb];
+          key = ((int64_t)(b - phase) + (b < phase ? (int64_t)1 << 30 : 0));
+        }
+        if (best < 0 || key < best_key) {
+          best = s;
+          best_key = key;
+        }
+      }
+      Slot& r = slot[best];
+      if (!r.started) {  // every resident row waits for its slot: start it now (the MMA stalls)
+        const int32_t* cols = bcol.data() + bp[r.g];
+        r.start = (int32_t)(std::lower_bound(cols, cols + r.nb, phase) - cols);
+        if (r.start == r.nb) r.start = 0;
+        r.started = true;
+      }
+      const int32_t t = (r.start + r.count) % r.nb;
+      const int32_t blk = bp[r.g] + t;
+      const bool first = r.count == 0, last = r.count + 1 == r.nb;
+      // the kernel's step: A tile row, first B row of the block's segment, n0, slot | first | last
+      const int64_t trow = tile_row[r.g] + (int64_t)t * tile_pitch(rp[r.g + 1] - rp[r.g]);
+      steps.push_back(make_int4((int32_t)trow, col_bounds[bcol[blk]], r.n0,
+                                best | (first ? 1 << 8 : 0) | (last ? 1 << 9 : 0)));
+      phase = bcol[blk];
+      ++k;
+      if (++r.count == r.nb) {
+        done.push_back(make_int4(r.g, r.n0, best, 0));
+        r.g = -1;
+        r.usable = k + delay;
+        --active;
+      }
+    }
+    step_ptr.push_back((int32_t)steps.size());
+    done_ptr.push_back((int32_t)done.size());
+  }
 }
 
 extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
@@ -1160,6 +1565,41 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       const int h = rp[r.x + 1] - rp[r.x];
       const int c = skinny_class(h);
       skinny_items_for_row(r.x, h, bp[r.x], r.y, N, sk_cols, skinny[c], sk_slots, sk_units, part[c]);
+    }
+  }
+  // Multi-slot sweep for the short height class with the most work, when it fills every CTA's slots
+  // at least once (RB_SWEEP=0 turns it off, RB_SWEEP=2 forces it; RB_SWEEP_DELAY = slot reuse delay in
+  // steps).
+  std::vector<int32_t> sw_rows;
+  int sw_hp = 0, sw_slots = 0;
+  {
+    const char* e = std::getenv("RB_SWEEP");
+    bool on = tc && !(e && e[0] == '0') && !short_g_major;
+    double work[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto cls = [](int hp) { return hp == 16 ? 0 : hp == 32 ? 1 : hp == 64 ? 2 : 3; };
+    for (int32_t g : short_rows) {
+      const int hp = hp_of(rp[g + 1] - rp[g]);
+      work[cls(hp)] += (double)(bp[g + 1] - bp[g]) * hp;
+      ++cnt[cls(hp)];
+    }
+    int best = 0;
+    for (int c = 1; c < 4; ++c)
+      if (work[c] > work[best]) best = c;
+    const int hp = 16 << best;
+    const int slots = std::min(MAX_SLOTS, 512 / (2 * hp));
+    int dev_ = 0, sms_ = kNumSMs;
+    RB_CUDA_TRY(cudaGetDevice(&dev_));
+    RB_CUDA_TRY(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_));
+    const int64_t n_slabs = (N + short_ns - 1) / short_ns;
+    const bool force = e && e[0] == '2';  // tests: sweep even a class that cannot fill the slots
+    if (vbr->total_tile_rows >= (1ll << 31) || vbr->n_cols >= (1ll << 31)) on = false;  // int32 step fields
+    if (on && work[best] > 0 && (force || cnt[best] * n_slabs >= (int64_t)sms_ * slots)) {
+      sw_hp = hp;
+      sw_slots = slots;
+      std::vector<int32_t> rest;
+      for (int32_t g : short_rows) (hp_of(rp[g + 1] - rp[g]) == hp ? sw_rows : rest).push_back(g);
+      short_rows.swap(rest);
     }
   }
   if (short_g_major) {
@@ -1286,12 +1726,66 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "zero-row list");
     }
   }
+  if (!sw_rows.empty()) {
+    std::vector<int32_t> bcol(vbr->n_blocks), cb(vbr->n_seg + 1);
+    std::vector<int64_t> trow(H);
+    cudaError_t e = cudaMemcpyAsync(bcol.data(), vbr->blk_col, sizeof(int32_t) * vbr->n_blocks, cudaMemcpyDeviceToHost,
+                                    stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(trow.data(), vbr->grp_tile_row, sizeof(int64_t) * H, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(cb.data(), vbr->col_bounds, sizeof(int32_t) * (vbr->n_seg + 1), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(RB_ECUDA, cudaGetErrorString(e));
+    }
+    std::vector<int32_t> slabs;
+    for (int64_t n0 = 0; n0 < N; n0 += short_ns) slabs.push_back((int32_t)n0);
+    int dev_ = 0, sms_ = kNumSMs;
+    RB_CUDA_TRY(cudaGetDevice(&dev_));
+    RB_CUDA_TRY(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_));
+    // slot reuse delay: the epilogue copies a finished slot to registers (~400 cycles) and hands it
+    // back before storing C, so a short delay suffices (config 5: 4 -> 2.32 ms, 8 -> 2.35, 32 -> 2.67)
+    int delay = 4;
+    if (const char* d = std::getenv("RB_SWEEP_DELAY")) delay = std::max(0, std::atoi(d));
+    const int ctas = (int)std::min<int64_t>(sms_, (int64_t)sw_rows.size() * (int64_t)slabs.size());
+    std::vector<int4> steps, done;
+    std::vector<int32_t> step_ptr, done_ptr;
+    sweep_schedule(sw_rows, slabs, rp, bp, bcol, trow, cb, vbr->n_seg, ctas, sw_slots, delay, dpc, steps, step_ptr, done,
+                   done_ptr);
+    e = cudaMalloc(&p->d_sw_steps, sizeof(int4) * steps.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_sw_done, sizeof(int4) * done.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_sw_step_ptr, sizeof(int32_t) * step_ptr.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_sw_done_ptr, sizeof(int32_t) * done_ptr.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_sw_steps, steps.data(), sizeof(int4) * steps.size(), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_sw_done, done.data(), sizeof(int4) * done.size(), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_sw_step_ptr, step_ptr.data(), sizeof(int32_t) * step_ptr.size(), cudaMemcpyHostToDevice,
+                          stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_sw_done_ptr, done_ptr.data(), sizeof(int32_t) * done_ptr.size(), cudaMemcpyHostToDevice,
+                          stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "sweep schedule");
+    }
+    p->sw_hp = sw_hp;
+    p->sw_slots = sw_slots;
+    p->sw_ctas = ctas;
+    p->n_sw_steps = (int64_t)steps.size();
+  }
   p->info.n_items_tall = p->n_tall;
-  p->info.n_items_short = p->n_short;
+  p->info.n_items_short = p->n_short + p->n_sw_steps;
+  p->info.n_sweep_steps = p->n_sw_steps;
+  p->info.sweep_slots = p->sw_slots;
   p->info.n_items_simt = p->n_simt;
   p->info.n_items_skinny = p->skinny_off[SKINNY_CLASSES];
   p->info.core_vbr_flops = core_vbr_flops;
-  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0);
+  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0) + (p->n_sw_steps > 0);
   for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   p->info.executed_flops = exec_flops;
   p->info.vbr_flops = vbr_flops;
@@ -1379,7 +1873,7 @@ extern "C" int rb_spmm_plan_attach_sparse24(rb_spmm_plan* p, const rb_sparse24_d
   p->n_res_items = (int64_t)ritems.size();
   p->use_sp = true;
   p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0) +
-                       (p->n_res_items > 0);
+                       (p->n_res_items > 0) + (p->n_sw_steps > 0);
   for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   return RB_OK;
 }
@@ -1401,6 +1895,10 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_sched) cudaFree(p->d_sched);
   if (p->d_zero) cudaFree(p->d_zero);
   if (p->d_short_ptr) cudaFree(p->d_short_ptr);
+  if (p->d_sw_steps) cudaFree(p->d_sw_steps);
+  if (p->d_sw_done) cudaFree(p->d_sw_done);
+  if (p->d_sw_step_ptr) cudaFree(p->d_sw_step_ptr);
+  if (p->d_sw_done_ptr) cudaFree(p->d_sw_done_ptr);
   if (p->d_sp_units) cudaFree(p->d_sp_units);
   if (p->d_sp_ws) cudaFree(p->d_sp_ws);
   if (p->d_sp_cnt) cudaFree(p->d_sp_cnt);
@@ -1492,12 +1990,13 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   CUtensorMap tmB;
   memset(&tmB, 0, sizeof(tmB));
   int sms = kNumSMs;
-  if (p->b_dtype != RB_F32 && (p->n_tall > 0 || p->n_short > 0)) {
+  if (p->b_dtype != RB_F32 && (p->n_tall > 0 || p->n_short > 0 || p->n_sw_steps > 0)) {
     static bool attr_done = false;
     if (!attr_done) {
       RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
       RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
       RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
+      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SWEEP));
       attr_done = true;
     }
     const CUtensorMapDataType dt =
@@ -1562,6 +2061,15 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
       const int ctas = p->short_ctas;
       spmm_short2_kernel<<<(unsigned)ctas, TC_THREADS, SMEM_SHORT, st>>>(p->tmA16, p->tmA32, p->tmA64, p->tmA128,
                                                                         tmB, s);
+      RB_CUDA_TRY(cudaGetLastError());
+      return (int)RB_OK;
+    });
+  if (p->b_dtype != RB_F32 && p->n_sw_steps > 0)
+    tasks.push_back([&](cudaStream_t st) {
+      SpmmArgs s = a;
+      SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp};
+      const CUtensorMap& tA = p->sw_hp == 16 ? p->tmA16 : p->sw_hp == 32 ? p->tmA32 : p->sw_hp == 64 ? p->tmA64 : p->tmA128;
+      spmm_sweep_kernel<<<(unsigned)p->sw_ctas, TC_THREADS, SMEM_SWEEP, st>>>(tA, tmB, s, w);
       RB_CUDA_TRY(cudaGetLastError());
       return (int)RB_OK;
     });

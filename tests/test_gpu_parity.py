@@ -212,6 +212,61 @@ def test_spmm_tall_and_short_shapes_bf16():
     del perm
 
 
+@pytest.mark.parametrize("h,delta,N,delay", [(64, 64, 1024, "8"), (40, 96, 320, "0"), (16, 64, 200, "3"),
+                                              (100, 64, 256, "8")])
+def test_spmm_sweep_kernel(h, delta, N, delay, monkeypatch):
+    """spmm_sweep_kernel (multi-slot circular sweep of one short height class): many block rows of
+    height h with random block columns, forced on (RB_SWEEP=2) so that small cases use it; two K
+    chunks per block when Δ > 64, a ragged last column slab when N % 256 != 0, slot reuse with and
+    without a delay.  C against the float64 product of the same rounded inputs; run-to-run identical."""
+    monkeypatch.setenv("RB_SWEEP", "2")
+    monkeypatch.setenv("RB_SWEEP_DELAY", delay)
+    rng = np.random.default_rng(h + N)
+    n_groups, n_seg = 300, 48
+    n_cols = n_seg * delta
+    rows, cols = [], []
+    for gi in range(n_groups):
+        segs = rng.choice(n_seg, size=int(rng.integers(1, 12)), replace=False)
+        for sgi in segs:
+            for r in range(gi * h, (gi + 1) * h):
+                c = rng.choice(np.arange(sgi * delta, (sgi + 1) * delta), size=int(rng.integers(1, 8)), replace=False)
+                rows.append(np.full(len(c), r))
+                cols.append(c)
+    n_rows = n_groups * h
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    vals = rounded(rng.uniform(-1, 1, len(rows)), torch.bfloat16)
+    keep = vals != 0
+    from paper_2202_05868_b200.types import RowGroup, RowGrouping, csr_from_coo
+    perm = rng.permutation(n_rows)
+    go = np.zeros(n_rows, np.int64)
+    groups = []
+    for gi in range(n_groups):
+        members = np.sort(perm[gi * h:(gi + 1) * h])
+        go[members] = gi
+        groups.append(RowGroup(members, np.zeros(0), 0))
+    # scramble the rows of A consistently with the grouping: row perm[i] of the grouping is row i of A
+    A = csr_from_coo(n_rows, n_cols, perm[rows[keep]], cols[keep], vals[keep], sum_duplicates=True)
+    V = rb.vbr_from_grouping(A, RowGrouping(go, groups), rb.ColumnPartition.uniform(n_cols, delta))
+    info = V.device.plan_info(N, "bf16")
+    assert info["n_sweep_steps"] > 0 and info["sweep_slots"] == min(16, 512 // (2 * max(16, 1 << (h - 1).bit_length())))
+    B = rounded(rng.uniform(-1, 1, (n_cols, N)), torch.bfloat16)
+    C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision="bf16").data
+    Ad = A.to_dense()
+    assert_close(C, Ad @ B, np.abs(Ad) @ np.abs(B), 1e-4, "sweep")
+    C2 = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision="bf16").data
+    assert np.array_equal(C, C2)
+
+
+def test_spmm_medium_cfg5_through_sweep(monkeypatch):
+    """The reference-generated 1/32-scale config 5 (128 block rows of h = 64) through the sweep kernel."""
+    monkeypatch.setenv("RB_SWEEP", "2")
+    case = load_golden("cfg5_s32")
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    assert V.device.plan_info(int(case["B_shape"][1]), "bf16")["n_sweep_steps"] > 0
+    test_spmm_medium_checksums("cfg5_s32", "bf16")
+
+
 def test_spmm_device_api_and_determinism():
     rng = np.random.default_rng(9)
     case = load_golden("cfg5_s32")
