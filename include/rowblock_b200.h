@@ -117,7 +117,12 @@ int rb_vbr_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx, 
  * tensor-core path, fp32 accumulate in TMEM) or RB_F32 (fp32 check path, FFMA).
  * A plan owns its work list (device memory it allocates and frees in _destroy).
  * Sharding: shard k of n_shards takes a contiguous, work-balanced range of the work list
- * (whole block-row M-tiles); each C row is produced by exactly one shard.             */
+ * (whole block-row M-tiles); each C row is produced by exactly one shard.
+ * Concurrency: rb_spmm_execute may be called on one plan from several host threads and streams.
+ * A plan holds device work counters and split-K partials that its kernels reset, so executions of
+ * ONE plan are serialised: each waits (cudaStreamWaitEvent, no host blocking) for the previous
+ * execution of the same plan when it is issued on a different stream.  Products meant to run
+ * concurrently need one plan each.                                                       */
 typedef struct rb_vbr_device {
   int64_t n_rows;
   int64_t n_cols;
@@ -230,6 +235,12 @@ int rb_group_stats(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const
  * dst[r, c] (row stride ldd, dtype dst_dtype) = src[r, c] (float64, row stride lds).   */
 int rb_convert_f64(const double* src, int64_t rows, int64_t cols, int64_t lds, void* dst, int32_t dst_dtype,
                    int64_t ldd, void* stream);
+/* rb_convert_f64 that also reports non-finite input: *nonfinite (device int32, caller-zeroed) is set
+ * to 1 if any element of src is NaN or +-Inf.  The drop-in spmm_vbr raises ValueError on that
+ * instead of returning the reference's NaN/Inf pattern (multiply.py:89 multiplies the dense block
+ * payloads, zeros included, while the kernels skip zero tile entries and pad tiles to 64 columns). */
+int rb_convert_f64_checked(const double* src, int64_t rows, int64_t cols, int64_t lds, void* dst, int32_t dst_dtype,
+                           int64_t ldd, int32_t* nonfinite, void* stream);
 /* float32 C → float64 (for DenseMatrix returns). */
 int rb_widen_f32(const float* src, int64_t rows, int64_t cols, int64_t lds, double* dst, int64_t ldd,
                  void* stream);

@@ -78,6 +78,7 @@ def lib():
         L.rb_spmm_execute.argtypes = [P, P, I64, P, I64, P]
         L.rb_spmm_plan_destroy.argtypes = [P]
         L.rb_convert_f64.argtypes = [P, I64, I64, I64, P, I32, I64, P]
+        L.rb_convert_f64_checked.argtypes = [P, I64, I64, I64, P, I32, I64, P, P]
         L.rb_widen_f32.argtypes = [P, I64, I64, I64, P, I64, P]
         L.rb_group_stats_workspace_size.argtypes = [I64, ctypes.POINTER(SZ)]
         L.rb_group_stats.argtypes = [I64, I64, P, P, P, I64, P, P, P, P, I64, ctypes.c_double, P, SZ, P, P, P, P,
@@ -98,7 +99,7 @@ def lib():
             getattr(L, name).restype = INT
         for name in ("rb_block_1sa_workspace_size", "rb_block_1sa", "rb_vbr_workspace_size", "rb_vbr_plan",
                      "rb_vbr_emit", "rb_spmm_plan_create", "rb_spmm_plan_info", "rb_spmm_execute",
-                     "rb_spmm_plan_destroy", "rb_convert_f64", "rb_widen_f32", "rb_group_stats_workspace_size",
+                     "rb_spmm_plan_destroy", "rb_convert_f64", "rb_convert_f64_checked", "rb_widen_f32", "rb_group_stats_workspace_size",
                      "rb_group_stats"):
             getattr(L, name).restype = INT
         _lib = L

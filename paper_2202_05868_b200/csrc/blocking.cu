@@ -1157,19 +1157,24 @@ __device__ bool spec_enumerate(const SGreedyArgs& a, const unsigned long long* s
     }
     __syncthreads();
     const int32_t nd = *s_ndefer;
-    if (!bs.flag && nd > 0) {
+    const bool hit = bs.flag != 0;
+    __syncthreads();  // the reads above complete before the warp verdicts below may set the flag
+    if (!hit && nd > 0) {
       for (int32_t k = threadIdx.x >> 5; k < nd; k += blockDim.x >> 5) {
         bool grows;
-        if (warp_eval(a, sP, s_defer[k], psize, cap, &grows) && lane == 0) bs.flag = 1;
+        if (warp_eval(a, sP, s_defer[k], psize, cap, &grows) && lane == 0) atomicExch(&bs.flag, 1);
       }
     }
-    // stop early (flag 3, not a hit of ours): another CTA found a hit for this seed or an earlier one
-    if (threadIdx.x == 0 && !bs.flag && stop &&
+    // stop early (flag 3, not a hit of ours): another CTA found a hit for this seed or an earlier one.
+    // CAS so that a hit (1) set concurrently by a warp verdict above is never overwritten.
+    if (threadIdx.x == 0 && !hit && stop &&
         (*((volatile const int32_t*)stop) || (stop_min && *((volatile const int32_t*)stop_min) < my_k)))
-      bs.flag = 3;
+      atomicCAS(&bs.flag, 0, 3);
     __syncthreads();
+    const int32_t f = bs.flag;  // every thread reads the flag of this iteration ...
     if (threadIdx.x == 0) *s_ndefer = 0;
-    if (bs.flag) break;  // uniform: read after the barrier
+    __syncthreads();  // ... before any thread can set it again in the next one (racecheck hazard)
+    if (f) break;     // uniform
   }
   __syncthreads();
   const bool found = bs.flag == 1;
@@ -1827,6 +1832,7 @@ extern "C" int rb_block_1sa(int64_t n, int64_t n_cols, int64_t nnz, const int64_
                             int pattern_update, int use_compression, void* workspace, size_t ws_bytes,
                             int64_t* group_of, int64_t* row_perm, int64_t* group_ptr, int64_t* seed_size,
                             int64_t* pattern_ptr, int64_t* pattern_idx, int64_t* n_groups, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_block_1sa");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   // MergePolicy validation (blocking.py:80-84)
   if (similarity != RB_JACCARD && similarity != RB_COSINE) return fail(RB_EINVAL, "unknown similarity");

@@ -66,14 +66,20 @@ __device__ __forceinline__ __half from_f64<__half>(double v) { return __double2h
 template <>
 __device__ __forceinline__ double from_f64<double>(double v) { return v; }
 
+// float64 -> kernel dtype; with `nonfinite`, any NaN / Inf in src sets *nonfinite = 1 (all writers
+// store the same value, so the race is benign).
 template <typename T>
 __global__ void convert_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t lds, T* dst,
-                               int64_t ldd) {
+                               int64_t ldd, int32_t* nonfinite) {
   const int64_t total = rows * cols;
+  bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / cols, c = i - r * cols;
-    dst[r * ldd + c] = from_f64<T>(src[r * lds + c]);
+    const double v = src[r * lds + c];
+    bad |= !isfinite(v);
+    dst[r * ldd + c] = from_f64<T>(v);
   }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *nonfinite = 1;
 }
 
 __global__ void widen_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds, double* dst,
@@ -92,21 +98,27 @@ using namespace rb;
 extern "C" const char* rb_last_error_string(void) { return g_last_error.c_str(); }
 extern "C" int rb_abi_version(void) { return 1; }
 
-extern "C" int rb_convert_f64(const double* src, int64_t rows, int64_t cols, int64_t lds, void* dst,
-                              int32_t dst_dtype, int64_t ldd, void* stream_) {
+extern "C" int rb_convert_f64_checked(const double* src, int64_t rows, int64_t cols, int64_t lds, void* dst,
+                                      int32_t dst_dtype, int64_t ldd, int32_t* nonfinite, void* stream_) {
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   if (rows < 0 || cols < 0 || lds < cols || ldd < cols) return fail(RB_EINVAL, "bad convert shape");
   if (rows * cols == 0) return RB_OK;
   const unsigned grid = (unsigned)std::min<int64_t>((rows * cols + 255) / 256, 148 * 32);
+  int32_t* f = nonfinite;
   switch (dst_dtype) {
-    case RB_F32: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (float*)dst, ldd); break;
-    case RB_BF16: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (__nv_bfloat16*)dst, ldd); break;
-    case RB_F16: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (__half*)dst, ldd); break;
-    case RB_F64: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (double*)dst, ldd); break;
+    case RB_F32: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (float*)dst, ldd, f); break;
+    case RB_BF16: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (__nv_bfloat16*)dst, ldd, f); break;
+    case RB_F16: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (__half*)dst, ldd, f); break;
+    case RB_F64: convert_kernel<<<grid, 256, 0, stream>>>(src, rows, cols, lds, (double*)dst, ldd, f); break;
     default: return fail(RB_EINVAL, "bad dtype");
   }
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
+}
+
+extern "C" int rb_convert_f64(const double* src, int64_t rows, int64_t cols, int64_t lds, void* dst,
+                              int32_t dst_dtype, int64_t ldd, void* stream_) {
+  return rb_convert_f64_checked(src, rows, cols, lds, dst, dst_dtype, ldd, nullptr, stream_);
 }
 
 extern "C" int rb_widen_f32(const float* src, int64_t rows, int64_t cols, int64_t lds, double* dst, int64_t ldd,

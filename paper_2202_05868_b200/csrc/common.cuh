@@ -5,6 +5,7 @@
 #include <string>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/rowblock_b200.h"
 
@@ -32,6 +33,15 @@ __host__ __device__ inline bool is_short_row(int32_t h) { return h <= 128; }
 // such a block row, reads hp rows from the pitch-spaced start: rows h..hp-1 then belong to the next
 // tiles (or are TMA zero fill) and only feed accumulator rows the epilogue never stores.
 __host__ __device__ inline int32_t tile_pitch(int32_t h) { return h <= 8 ? h : hp_of(h); }
+
+// NVTX range over one C-ABI call (1-SA, VBR build, SpMM, ...): named stages on an nsys / ncu timeline;
+// header-only NVTX v3, a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Thread-local error string for rb_last_error_string().
 void set_error(const std::string& s);

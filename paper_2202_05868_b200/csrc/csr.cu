@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "spmm_skinny.cuh"
 
@@ -19,6 +21,12 @@ struct rb_csr_plan {
   float* d_ws = nullptr;
   int32_t* d_cnt = nullptr;
   unsigned long long* d_sched = nullptr;
+  // executions of one plan are serialised (its work counters and split partials are reset by the
+  // kernels themselves): host threads through `mu`, streams through the `done` event
+  mutable std::mutex mu;
+  mutable cudaEvent_t done = nullptr;
+  mutable cudaStream_t done_stream = nullptr;
+  mutable bool done_valid = false;
 };
 
 using namespace rb;
@@ -29,6 +37,7 @@ extern "C" int rb_csr_plan_destroy(rb_csr_plan* p) {
   if (p->d_ws) cudaFree(p->d_ws);
   if (p->d_cnt) cudaFree(p->d_cnt);
   if (p->d_sched) cudaFree(p->d_sched);
+  if (p->done) cudaEventDestroy(p->done);
   delete p;
   return RB_OK;
 }
@@ -94,6 +103,7 @@ extern "C" int rb_csr_plan_create(int64_t n_rows, int64_t n_cols, const int64_t*
 
 extern "C" int rb_csr_execute(const rb_csr_plan* p, const int64_t* row_ptr, const int64_t* col_idx,
                               const double* values, const void* B, int64_t ldb, float* C, int64_t ldc, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_csr_execute");
   if (!p) return fail(RB_EINVAL, "null plan");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   if (ldb < p->N || ldc < p->N) return fail(RB_EINVAL, "leading dimension smaller than N");
@@ -112,5 +122,12 @@ extern "C" int rb_csr_execute(const rb_csr_plan* p, const int64_t* row_ptr, cons
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
   CsrArgs c{row_ptr, col_idx, values, nullptr, nullptr};
-  return launch_csr(a, c, p->b_dtype, p->d_sched, stream);
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (!p->done) RB_CUDA_TRY(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+  if (p->done_valid && p->done_stream != stream) RB_CUDA_TRY(cudaStreamWaitEvent(stream, p->done, 0));
+  if (int rc = launch_csr(a, c, p->b_dtype, p->d_sched, stream)) return rc;
+  RB_CUDA_TRY(cudaEventRecord(p->done, stream));
+  p->done_stream = stream;
+  p->done_valid = true;
+  return RB_OK;
 }

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <functional>
+#include <mutex>
 #include <queue>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -1118,6 +1119,12 @@ static int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt
                         CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(RB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  {  // a driver-API call: make the device's primary context current in this host thread (a thread
+     // whose first CUDA call this is has none yet -> CUDA_ERROR_INVALID_CONTEXT)
+    int dev = 0;
+    RB_CUDA_TRY(cudaGetDevice(&dev));
+    RB_CUDA_TRY(cudaSetDevice(dev));
+  }
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(RB_EINVAL, "TMA base must be 16-byte aligned");
   if (row_bytes % 16 != 0) return fail(RB_EINVAL, "TMA row stride must be a multiple of 16 bytes");
   cuuint64_t dims[2] = {inner, outer};
@@ -1210,6 +1217,14 @@ struct rb_spmm_plan {
   rb::SkinnyItem* d_res_items = nullptr;
   int64_t n_res_items = 0;
   unsigned long long* d_res_sched = nullptr;
+  // Executions of one plan are serialised: the work counters, split partials and schedules above
+  // are per-plan device state that every launch resets itself, so two executions must never
+  // overlap.  `mu` makes rb_spmm_execute safe from several host threads; `done` (recorded at the
+  // end of every execution) is waited on by the next execution when it comes on another stream.
+  mutable std::mutex mu;
+  mutable cudaEvent_t done = nullptr;
+  mutable cudaStream_t done_stream = nullptr;
+  mutable bool done_valid = false;
   // fork/join streams of rb_spmm_execute (created on first use)
   mutable bool aux_ready = false;
   mutable cudaStream_t aux[rb::kAuxStreams] = {};
@@ -1457,6 +1472,7 @@ static void sweep_schedule(const std::vector<int32_t>& rows, const std::vector<i
 
 extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
                                    int32_t n_shards, rb_spmm_plan** out, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_spmm_plan_create");
   if (!vbr || !out) return fail(RB_EINVAL, "null argument");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const bool tc = (b_dtype == RB_BF16 || b_dtype == RB_F16);
@@ -1908,14 +1924,48 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
     for (int l = 0; l < kAuxStreams; ++l) cudaStreamDestroy(p->aux[l]);
     for (int l = 0; l <= kAuxStreams; ++l) cudaEventDestroy(p->ev[l]);
   }
+  if (p->done) cudaEventDestroy(p->done);
   delete p;
   return RB_OK;
 }
 
+// Kernel attributes are per device: set them once per device ordinal (thread-safe).
+static int ensure_kernel_attributes() {
+  static std::mutex m;
+  static bool done[64] = {};
+  int dev = 0;
+  RB_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(m);
+  if (dev >= 0 && dev < 64 && done[dev]) return RB_OK;
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SWEEP));
+  if (dev >= 0 && dev < 64) done[dev] = true;
+  return RB_OK;
+}
+
+static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
+                               cudaStream_t stream);
+
 extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
                                void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_spmm_execute");
   if (!p) return fail(RB_EINVAL, "null plan");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (!p->done) RB_CUDA_TRY(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+  if (p->done_valid && p->done_stream != stream) RB_CUDA_TRY(cudaStreamWaitEvent(stream, p->done, 0));
+  const int rc = spmm_execute_locked(p, B, ldb, C, ldc, stream);
+  if (rc) return rc;
+  RB_CUDA_TRY(cudaEventRecord(p->done, stream));
+  p->done_stream = stream;
+  p->done_valid = true;
+  return RB_OK;
+}
+
+static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
+                               cudaStream_t stream) {
   if (ldc < p->N || ldb < p->N) return fail(RB_EINVAL, "leading dimension smaller than N");
   if (!C && p->v.n_rows > 0) return fail(RB_EINVAL, "null C");
   SpmmArgs a;
@@ -1991,14 +2041,7 @@ extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb
   memset(&tmB, 0, sizeof(tmB));
   int sms = kNumSMs;
   if (p->b_dtype != RB_F32 && (p->n_tall > 0 || p->n_short > 0 || p->n_sw_steps > 0)) {
-    static bool attr_done = false;
-    if (!attr_done) {
-      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
-      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
-      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
-      RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SWEEP));
-      attr_done = true;
-    }
+    if (int rc = ensure_kernel_attributes()) return rc;
     const CUtensorMapDataType dt =
         p->b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     int rc = make_tmap_2d(&tmB, B, dt, (uint64_t)p->N, (uint64_t)p->v.n_cols, (uint64_t)ldb * 2, 64, 64);

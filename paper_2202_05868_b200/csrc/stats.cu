@@ -92,6 +92,7 @@ extern "C" int rb_group_stats(int64_t n_rows, int64_t n_cols, const int64_t* row
                               int64_t* stored_cols, int64_t* element_nnz, int64_t* quotient_nnz, uint8_t* ok,
                               int64_t* stored_area, int64_t* n_blocks, int64_t* height_sum, int64_t* n_violations,
                               void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_group_stats");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   if (n_rows < 0 || n_groups < 0 || !(tau >= 0.0 && tau <= 1.0)) return fail(RB_EINVAL, "bad arguments");
   if (!stored_area || !n_blocks || !height_sum || !n_violations) return fail(RB_EINVAL, "null total");

@@ -250,6 +250,7 @@ extern "C" int rb_vbr_plan(int64_t n_rows, int64_t n_cols, const int64_t* row_pt
                            const int64_t* row_partition, int64_t H, void* workspace, size_t ws_bytes, int32_t* perm32,
                            int32_t* rpart32, int32_t* blk_ptr, int64_t* grp_tile_row, int32_t* bounds32,
                            int64_t* n_blocks, int64_t* total_tile_rows, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_vbr_plan");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   if (n_rows < 0 || H < 0 || !n_blocks || !total_tile_rows) return fail(RB_EINVAL, "bad arguments");
   if (n_rows >= (int64_t(1) << 31)) return fail(RB_EUNSUPPORTED, "n_rows must be < 2^31");
@@ -308,6 +309,7 @@ extern "C" int rb_vbr_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t
                            const int32_t* perm32, const int32_t* rpart32, const int32_t* blk_ptr,
                            const int64_t* grp_tile_row, int32_t* blk_col, void* tiles, int32_t tile_dtype, int32_t dp,
                            int64_t total_tile_rows, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_vbr_emit");
   (void)perm32;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const int64_t W = words_of(n_seg);

@@ -22,8 +22,13 @@ __all__ = ["spmm_vbr", "spmm_vbr_many", "spmm_vbr_device", "spmm_csr", "upload_d
            "pinned_dense"]
 
 
-def upload_dense(B, precision: str, device=None) -> torch.Tensor:
-    """Host float64 [K, N] → device tensor of the kernel dtype with a 16-byte aligned row stride."""
+NONFINITE_B = ("B contains NaN or Inf: the reference propagates them through the dense block payloads "
+               "(multiply.py:89, zeros included), which the GPU path does not reproduce, so it refuses")
+
+
+def upload_dense(B, precision: str, device=None, nonfinite: torch.Tensor | None = None) -> torch.Tensor:
+    """Host float64 [K, N] → device tensor of the kernel dtype with a 16-byte aligned row stride.
+    ``nonfinite``: optional device int32[1] (zeroed by the caller) set to 1 if B holds NaN / Inf."""
     dev = device or L.require_cuda()
     a = np.ascontiguousarray(np.asarray(B.data if hasattr(B, "data") else B, dtype=np.float64))
     K, N = a.shape
@@ -31,7 +36,8 @@ def upload_dense(B, precision: str, device=None) -> torch.Tensor:
     ld = (N + 7) // 8 * 8
     src = host_tensor(a).to(dev)
     buf = torch.empty((K, ld), dtype=L.TORCH_DTYPE[td], device=dev)
-    L.check(L.lib().rb_convert_f64(L.ptr(src), K, N, N, L.ptr(buf), td, ld, L.stream_handle()))
+    flag = L.ptr(nonfinite) if nonfinite is not None else None
+    L.check(L.lib().rb_convert_f64_checked(L.ptr(src), K, N, N, L.ptr(buf), td, ld, flag, L.stream_handle()))
     return buf[:, :N]
 
 
@@ -68,11 +74,15 @@ def spmm_vbr(V, B, threads: int = 1, *, precision: str | None = None) -> DenseMa
     N = B.n_cols
     if V.n_rows == 0 or N == 0:
         return DenseMatrix(V.n_rows, N, np.zeros((V.n_rows, N)))
-    Bd = upload_dense(B, prec)
+    bad = torch.zeros(1, dtype=torch.int32, device=L.require_cuda())
+    Bd = upload_dense(B, prec, nonfinite=bad)
     C32 = dv.spmm(Bd, precision=prec)
     C64 = torch.empty((V.n_rows, N), dtype=torch.float64, device=C32.device)
     L.check(L.lib().rb_widen_f32(L.ptr(C32), V.n_rows, N, N, L.ptr(C64), N, L.stream_handle()))
-    return DenseMatrix(V.n_rows, N, C64.cpu().numpy())
+    C = C64.cpu().numpy()  # synchronises: the flag below is final
+    if int(bad.item()):
+        raise ValueError(NONFINITE_B)
+    return DenseMatrix(V.n_rows, N, C)
 
 
 def pinned_dense(n_rows: int, n_cols: int) -> torch.Tensor:
@@ -105,6 +115,7 @@ class SpmmPipeline:
         self.s_in, self.s_comp, self.s_out = (torch.cuda.Stream(dev) for _ in range(3))
         mk = lambda: [torch.cuda.Event() for _ in range(depth)]  # noqa: E731
         self.ev_in, self.ev_comp, self.ev_out = mk(), mk(), mk()
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)  # set by any step's B conversion
         self.used = [False] * depth
         self.dv.plan(self.N, self.prec, stream=self.s_comp)  # plan creation outside the steady state
 
@@ -118,8 +129,8 @@ class SpmmPipeline:
             if self.used[i]:
                 self.s_in.wait_event(self.ev_comp[i])  # buffers of step k - depth consumed
             self.b64[i].copy_(B_host, non_blocking=True)
-            L.check(lib.rb_convert_f64(L.ptr(self.b64[i]), self.K, self.N, self.N, L.ptr(self.bk[i]), self.td,
-                                       self.ld, L.stream_handle(self.s_in)))
+            L.check(lib.rb_convert_f64_checked(L.ptr(self.b64[i]), self.K, self.N, self.N, L.ptr(self.bk[i]),
+                                               self.td, self.ld, L.ptr(self.nonfinite), L.stream_handle(self.s_in)))
             self.ev_in[i].record(self.s_in)
         with torch.cuda.stream(self.s_comp):
             self.s_comp.wait_event(self.ev_in[i])
@@ -137,6 +148,12 @@ class SpmmPipeline:
 
     def synchronize(self) -> None:
         self.s_out.synchronize()
+
+    def check_finite(self) -> None:
+        """Raise ValueError if any B converted so far held NaN / Inf (see NONFINITE_B)."""
+        self.s_in.synchronize()
+        if int(self.nonfinite.item()):
+            raise ValueError(NONFINITE_B)
 
 
 def spmm_vbr_many(V, Bs, threads: int = 1, *, precision: str | None = None, out=None) -> list:
@@ -158,4 +175,5 @@ def spmm_vbr_many(V, Bs, threads: int = 1, *, precision: str | None = None, out=
         src = B if isinstance(B, torch.Tensor) else host_tensor(np.asarray(B.data, dtype=np.float64))
         pipe.step(k, src, outs[k])
     pipe.synchronize()
+    pipe.check_finite()
     return [DenseMatrix(V.n_rows, N, o.numpy()) for o in outs]

@@ -75,3 +75,19 @@ def test_shard_balance_config_like():
         w = np.diff(bp) + 1.0
         loads = [w[b // 64:e // 64].sum() for b, e in ranges]
         assert max(loads) - min(loads) <= 2 * w.max()
+
+
+def test_csr_validation_messages_match_reference():
+    """CsrMatrix.validate raises the reference's messages (matrix.py:79-96), including the first
+    offending row for unsorted columns."""
+    import pytest
+
+    from paper_2202_05868_b200.types import CsrMatrix
+
+    cases = [(([0, 2, 4, 6], [0, 1, 3, 2, 0, 1]), "row 1: columns not strictly increasing"),
+             (([0, 0, 3, 3], [1, 1, 2]), "row 1: columns not strictly increasing"),
+             (([0, 3], [2, 1, 0]), "row 0: columns not strictly increasing"),
+             (([0, 2], [0, 7]), "column index out of range")]
+    for (rp, ci), msg in cases:
+        with pytest.raises(ValueError, match=msg):
+            CsrMatrix(len(rp) - 1, 4, np.array(rp), np.array(ci), np.ones(len(ci))).validate()

@@ -283,6 +283,78 @@ def test_spmm_device_api_and_determinism():
     del rng
 
 
+@pytest.mark.parametrize("name,N,split", [("rmat12_t3", 64, None), ("cfg5_s32", 256, None), ("cfg4_s8", 512, "2")])
+def test_one_plan_on_two_streams(name, N, split, monkeypatch):
+    """One DeviceVbr (one cached plan per N) driven from two streams and two host threads at once:
+    the plan's self-resetting work counters and split partials (skinny scheduler, split hub rows,
+    tall split-K tail) must not be shared by overlapping executions (rowblock_b200.h: executions
+    of one plan are serialised on the device).  Each result equals the single-stream result."""
+    import threading
+
+    if split:
+        monkeypatch.setenv("RB_TALL_SPLIT", split)
+    case = load_golden(name)
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    dv = V.device
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Bs = [torch.rand((A.n_cols, N), device="cuda", generator=g).to(torch.bfloat16) for _ in range(4)]
+    refs = [dv.spmm(B, precision="bf16").clone() for B in Bs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [torch.empty_like(r) for r in refs]
+    for rep in range(3):
+        for k, B in enumerate(Bs):  # alternate streams without host synchronisation
+            st = streams[k % 2]
+            with torch.cuda.stream(st):
+                dv.spmm(B, out=outs[k], precision="bf16", stream=st)
+        torch.cuda.synchronize()
+        for k in range(len(Bs)):
+            assert torch.equal(outs[k], refs[k]), (rep, k)
+    # two host threads, each on its own stream
+    errs = []
+
+    def worker(k):
+        try:
+            st = streams[k % 2]
+            with torch.cuda.stream(st):
+                for _ in range(4):
+                    dv.spmm(Bs[k], out=outs[k], precision="bf16", stream=st)
+            st.synchronize()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(k,)) for k in range(len(Bs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs
+    for k in range(len(Bs)):
+        assert torch.equal(outs[k], refs[k]), k
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_b_raises(bad):
+    """The reference propagates NaN / Inf of B through its dense block payloads (multiply.py:89);
+    the GPU path skips zero tile entries and pads tiles, so it cannot reproduce that pattern and
+    raises ValueError instead of returning a different one (spmm_vbr and spmm_vbr_many)."""
+    case = load_golden("cfg1_full")
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    B = np.random.default_rng(3).random((A.n_cols, 32))
+    B[17, 5] = bad
+    for prec in ("bf16", "fp32"):
+        with pytest.raises(ValueError, match="NaN or Inf"):
+            rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision=prec)
+    ok = np.random.default_rng(4).random((A.n_cols, 32))
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        rb.spmm_vbr_many(V, [rb.DenseMatrix.from_array(ok), rb.DenseMatrix.from_array(B)], precision="bf16")
+    C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(ok), precision="bf16").data  # finite B still works
+    assert np.isfinite(C).all()
+
+
 def test_errors_map_to_reference_exceptions():
     A = rb.csr_from_triplets(4, 6, [(0, 0, 1.0), (0, 1, 1.0), (1, 3, 1.0), (2, 2, 1.0), (3, 4, 1.0), (3, 5, 1.0)])
     q = rb.ColumnPartition.uniform(6, 3)
@@ -616,3 +688,35 @@ def test_spmm_shard_plans_cover_rows_and_match_full(precision, world):
     assert not torch.isnan(C).any(), "a row was not written by any shard"
     err = (C.double() - full.double()).abs().max().item()
     assert err <= 1e-5 * max(1.0, full.abs().max().item())
+
+
+@pytest.mark.parametrize("precision,world", [("bf16", 4), ("bf16", 8), ("fp32", 8)])
+def test_spmm_shard_plans_split_hub_rows(precision, world):
+    """Plans with 4+ shards cut skinny block rows into 128-block (4 ranks) / 64-block (8 ranks) parts
+    reduced in part order by the last-arriving part.  Skinny rows here hold ~200 blocks (19,200
+    columns, Δ=64), so every shard splits them; all rows written, equal to the single plan."""
+    from paper_2202_05868_b200 import _lib as L
+    from paper_2202_05868_b200.device import DeviceCsr, DeviceVbr
+
+    rng = np.random.default_rng(77 + world)
+    heights = [1, 2, 4, 1, 3, 1, 1, 2, 4, 1] * 3
+    n_cols = 64 * 300
+    A, perm, rp = _grouped_matrix(rng, heights, n_cols, 64, 0.02)
+    q = rb.ColumnPartition.uniform(n_cols, 64)
+    dt = L.TORCH_DTYPE[L.PRECISION[precision]]
+    N = 128
+    Bh = rounded(rng.uniform(-1, 1, (n_cols, N)), dt if dt != torch.float32 else torch.bfloat16)
+    Bd = torch.from_numpy(Bh).to(dt).cuda()
+    dv = DeviceVbr.build(DeviceCsr.from_host(A, "cuda"), q, perm, rp, dtypes=(precision,))
+    _, bp, _ = dv.host_structure()
+    assert np.diff(bp).max() > 128  # hub rows that the 4/8-rank part sizes cut
+    full = dv.spmm(Bd, precision=precision)
+    C = torch.full_like(full, float("nan"))
+    for k in range(world):
+        dv.spmm(Bd, out=C, precision=precision, shard=k, n_shards=world)
+    torch.cuda.synchronize()
+    assert not torch.isnan(C).any(), "a row was not written by any shard"
+    err = (C.double() - full.double()).abs().max().item()
+    assert err <= 1e-5 * max(1.0, full.abs().max().item())
+    ref = torch.from_numpy(A.to_dense() @ Bh).cuda()
+    assert ((C.double() - ref).abs().max() <= 1e-4 * max(1.0, ref.abs().max().item())).item()
