@@ -161,6 +161,12 @@ int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t 
                         int32_t n_shards, rb_spmm_plan** plan, void* stream);
 int rb_spmm_plan_info(const rb_spmm_plan* plan, rb_spmm_info* info);
 int rb_spmm_execute(const rb_spmm_plan* plan, const void* B, int64_t ldb, float* C, int64_t ldc, void* stream);
+/* float64 path (plan made with b_dtype RB_F64 over RB_F64 tiles): C float64.  Every block row runs
+ * on a CUDA-core FP64 kernel that multiplies the dense block payloads over exactly their segment
+ * width, zeros included, as multiply.py:89 does — results within float64 rounding of the reference
+ * and the same NaN / Inf propagation. */
+int rb_spmm_execute_f64(const rb_spmm_plan* plan, const double* B, int64_t ldb, double* C, int64_t ldc,
+                        void* stream);
 int rb_spmm_plan_destroy(rb_spmm_plan* plan);
 /* 2:4 sparse tensor-core form of the tall block rows (sparse24.cu): stage = 128 logical K of a
  * block row's padded block sequence; 64 compressed values + 4 TMEM metadata words per tile row and

@@ -19,7 +19,7 @@ RB_F32, RB_BF16, RB_F16, RB_F64 = 0, 1, 2, 3
 RB_JACCARD, RB_COSINE = 0, 1
 
 TORCH_DTYPE = {RB_F32: torch.float32, RB_BF16: torch.bfloat16, RB_F16: torch.float16, RB_F64: torch.float64}
-PRECISION = {"bf16": RB_BF16, "fp16": RB_F16, "fp32": RB_F32}
+PRECISION = {"bf16": RB_BF16, "fp16": RB_F16, "fp32": RB_F32, "fp64": RB_F64}
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -76,6 +76,7 @@ def lib():
         L.rb_spmm_plan_create.argtypes = [ctypes.POINTER(VbrDevice), I64, I32, I32, I32, ctypes.POINTER(P), P]
         L.rb_spmm_plan_info.argtypes = [P, ctypes.POINTER(SpmmInfo)]
         L.rb_spmm_execute.argtypes = [P, P, I64, P, I64, P]
+        L.rb_spmm_execute_f64.argtypes = [P, P, I64, P, I64, P]
         L.rb_spmm_plan_destroy.argtypes = [P]
         L.rb_convert_f64.argtypes = [P, I64, I64, I64, P, I32, I64, P]
         L.rb_convert_f64_checked.argtypes = [P, I64, I64, I64, P, I32, I64, P, P]
@@ -98,7 +99,7 @@ def lib():
         for name in ("rb_csr_plan_create", "rb_csr_execute", "rb_csr_plan_destroy"):
             getattr(L, name).restype = INT
         for name in ("rb_block_1sa_workspace_size", "rb_block_1sa", "rb_vbr_workspace_size", "rb_vbr_plan",
-                     "rb_vbr_emit", "rb_spmm_plan_create", "rb_spmm_plan_info", "rb_spmm_execute",
+                     "rb_vbr_emit", "rb_spmm_plan_create", "rb_spmm_plan_info", "rb_spmm_execute", "rb_spmm_execute_f64",
                      "rb_spmm_plan_destroy", "rb_convert_f64", "rb_convert_f64_checked", "rb_widen_f32", "rb_group_stats_workspace_size",
                      "rb_group_stats"):
             getattr(L, name).restype = INT

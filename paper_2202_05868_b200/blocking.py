@@ -9,6 +9,7 @@ round trip.
 
 from __future__ import annotations
 
+from . import _forkproxy
 from .device import DeviceCsr, block_1sa_device
 from .types import ColumnPartition, MergePolicy, RowGrouping
 
@@ -19,6 +20,8 @@ def block_1sa(A, partition: ColumnPartition, policy: MergePolicy, use_compressio
     """Group the rows of A by greedy similarity against the partition (bit-exact with the reference)."""
     if partition.n_cols != A.n_cols:
         raise ValueError("partition inconsistent with matrix dimensions")
+    if _forkproxy.in_bad_fork():  # forked pool worker of a CUDA parent: run in a spawned helper
+        return _forkproxy.call("block_1sa", A, partition, policy, use_compression)
     dA = DeviceCsr.from_host(A)
     dg = block_1sa_device(dA, partition, policy, use_compression)
     dg.csr = dA

@@ -9,13 +9,14 @@ _PRECISION = os.environ.get("ROWBLOCK_B200_PRECISION", "bf16")
 
 def default_precision() -> str:
     """Kernel precision used by vbr_from_grouping / spmm_vbr when none is given:
-    "bf16" (tcgen05, default), "fp16" (tcgen05) or "fp32" (check path)."""
+    "bf16" (tcgen05, default), "fp16" (tcgen05), "fp32" (check path) or "fp64" (float64 CUDA-core
+    path: the reference's arithmetic, ~1e-15 relative, NaN / Inf of B propagated as multiply.py:89)."""
     return _PRECISION
 
 
 def set_default_precision(p: str) -> None:
     global _PRECISION
-    if p not in ("bf16", "fp16", "fp32"):
+    if p not in ("bf16", "fp16", "fp32", "fp64"):
         raise ValueError(f"unknown precision {p!r}")
     _PRECISION = p
 

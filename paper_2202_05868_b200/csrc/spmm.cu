@@ -1038,9 +1038,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // ------------------------------------------------------------------------------------------
 // fp32 check path: CTA = (g, 8-row chunk r0, 128-col chunk n0); thread = one C column.
 // Per row the accumulation order is blocks ascending, then k ascending (fixed, deterministic).
-__global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, const float* __restrict__ tiles,
-                                                                   int32_t dp, const float* __restrict__ B,
-                                                                   int64_t ldb) {
+// T = float: the fp32 check path for h > 8.  T = double: the fp64 path (every block row), which
+// multiplies exactly the segment width with the zeros of the dense block payload included, so it
+// reproduces the reference's float64 arithmetic and its NaN / Inf propagation (multiply.py:89).
+template <typename T>
+__global__ void __launch_bounds__(SIMT_COLS) spmm_simt_kernel(SpmmArgs a, const T* __restrict__ tiles, int32_t dp,
+                                                              const T* __restrict__ B, int64_t ldb, T* C) {
   const int4 it = a.items[blockIdx.x];
   const int g = it.x, r0 = it.y, n0 = it.z;
   const int p0 = a.row_partition[g];
@@ -1049,32 +1052,32 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_f32_kernel(SpmmArgs a, co
   const int rows = min(SIMT_ROWS, h - r0);
   const int n = n0 + threadIdx.x;
   const bool nv = n < a.N;
-  float acc[SIMT_ROWS];
+  T acc[SIMT_ROWS];
 #pragma unroll
-  for (int r = 0; r < SIMT_ROWS; ++r) acc[r] = 0.f;
+  for (int r = 0; r < SIMT_ROWS; ++r) acc[r] = T(0);
   const int b0 = a.blk_ptr[g], b1 = a.blk_ptr[g + 1];
   const int64_t base = a.grp_tile_row[g];
   for (int b = b0; b < b1; ++b) {
     const int s = a.blk_col[b];
     const int k0 = a.col_bounds[s], w = a.col_bounds[s + 1] - k0;
-    const float* t = tiles + (base + (int64_t)(b - b0) * hp + r0) * dp;
-    const float* bp = B + (int64_t)k0 * ldb + n;
+    const T* t = tiles + (base + (int64_t)(b - b0) * hp + r0) * dp;
+    const T* bp = B + (int64_t)k0 * ldb + n;
     if (rows == 1) {  // most short block rows have h = 1 (config 1): no wasted FMAs on padding rows
       for (int k = 0; k < w; ++k) {
-        const float bv = nv ? __ldg(bp + (int64_t)k * ldb) : 0.f;
-        acc[0] = __fmaf_rn(__ldg(t + k), bv, acc[0]);
+        const T bv = nv ? __ldg(bp + (int64_t)k * ldb) : T(0);
+        acc[0] = fma(__ldg(t + k), bv, acc[0]);
       }
     } else {
       for (int k = 0; k < w; ++k) {
-        const float bv = nv ? __ldg(bp + (int64_t)k * ldb) : 0.f;
+        const T bv = nv ? __ldg(bp + (int64_t)k * ldb) : T(0);
 #pragma unroll
         for (int r = 0; r < SIMT_ROWS; ++r)
-          if (r < rows) acc[r] = __fmaf_rn(__ldg(t + r * dp + k), bv, acc[r]);
+          if (r < rows) acc[r] = fma(__ldg(t + r * dp + k), bv, acc[r]);
       }
     }
   }
   if (nv) {
-    for (int r = 0; r < rows; ++r) a.C[(int64_t)a.row_perm[p0 + r0 + r] * a.ldc + n] = acc[r];
+    for (int r = 0; r < rows; ++r) C[(int64_t)a.row_perm[p0 + r0 + r] * a.ldc + n] = acc[r];
   }
 }
 
@@ -1476,9 +1479,11 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   if (!vbr || !out) return fail(RB_EINVAL, "null argument");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const bool tc = (b_dtype == RB_BF16 || b_dtype == RB_F16);
-  if (!tc && b_dtype != RB_F32) return fail(RB_EUNSUPPORTED, "B dtype must be bf16, f16 or f32");
+  const bool f64 = b_dtype == RB_F64;
+  if (!tc && !f64 && b_dtype != RB_F32) return fail(RB_EUNSUPPORTED, "B dtype must be bf16, f16, f32 or f64");
   if (tc && vbr->tile_dtype != b_dtype) return fail(RB_EINVAL, "tile dtype must equal B dtype");
-  if (!tc && vbr->tile_dtype != RB_F32) return fail(RB_EINVAL, "fp32 path needs fp32 tiles");
+  if (!tc && !f64 && vbr->tile_dtype != RB_F32) return fail(RB_EINVAL, "fp32 path needs fp32 tiles");
+  if (f64 && vbr->tile_dtype != RB_F64) return fail(RB_EINVAL, "fp64 path needs fp64 tiles");
   if (tc && (vbr->dp <= 0 || vbr->dp % 64 != 0)) return fail(RB_EINVAL, "dp must be a positive multiple of 64");
   if (N <= 0 || N > (1ll << 30)) return fail(RB_EINVAL, "bad n_dense_cols");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(RB_EINVAL, "bad shard");
@@ -1511,6 +1516,7 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
   // be >= 15/16 padding rows.  fp32 path: h <= 8; tensor path: h <= 4 (RB_SKINNY_H overrides, 0..8).
   int skinny_h = tc ? 4 : 8;
   if (const char* sk = std::getenv("RB_SKINNY_H")) skinny_h = std::max(0, std::min(8, std::atoi(sk)));
+  if (f64) skinny_h = 0;  // fp64: every block row on the float64 SIMT kernel
   const int sk_cols = skinny_cols(b_dtype, N);
   std::vector<SkinnyItem> skinny[SKINNY_CLASSES];
   std::vector<int32_t> zero_rows;  // permuted positions of the rows of empty block rows
@@ -1948,9 +1954,25 @@ static int ensure_kernel_attributes() {
 static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
                                cudaStream_t stream);
 
+static int spmm_execute_entry(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
+                              void* stream_);
+
 extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
                                void* stream_) {
   rb::NvtxRange nvtx_range_("rb_spmm_execute");
+  if (p && p->b_dtype == RB_F64) return fail(RB_EINVAL, "fp64 plan: use rb_spmm_execute_f64");
+  return spmm_execute_entry(p, B, ldb, C, ldc, stream_);
+}
+
+extern "C" int rb_spmm_execute_f64(const rb_spmm_plan* p, const double* B, int64_t ldb, double* C, int64_t ldc,
+                                   void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_spmm_execute_f64");
+  if (p && p->b_dtype != RB_F64) return fail(RB_EINVAL, "rb_spmm_execute_f64 needs a plan made for RB_F64");
+  return spmm_execute_entry(p, B, ldb, reinterpret_cast<float*>(C), ldc, stream_);
+}
+
+static int spmm_execute_entry(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
+                              void* stream_) {
   if (!p) return fail(RB_EINVAL, "null plan");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   std::lock_guard<std::mutex> lk(p->mu);
@@ -1997,7 +2019,9 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
   if (p->n_zero > 0)
     tasks.push_back([&](cudaStream_t st) {
       const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
-      zero_rows_kernel<<<grid, 256, 0, st>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc, (int32_t)p->N);
+      // fp64 C: a row of N doubles is 2N zero floats
+      const int w = p->b_dtype == RB_F64 ? 2 : 1;
+      zero_rows_kernel<<<grid, 256, 0, st>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc * w, (int32_t)p->N * w);
       RB_CUDA_TRY(cudaGetLastError());
       return RB_OK;
     });
@@ -2026,21 +2050,27 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       return launch_skinny(kc, p->b_dtype, c, p->d_sched + 2 * c, st);
     });
   }
-  if (p->b_dtype == RB_F32 && p->n_simt > 0)
+  if ((p->b_dtype == RB_F32 || p->b_dtype == RB_F64) && p->n_simt > 0)
     tasks.push_back([&](cudaStream_t st) {
       SpmmArgs s = a;
       s.items = p->d_items + 2 * p->n_tall + p->n_short;
       s.n_items = (int32_t)p->n_simt;
       s.dp_chunks = 1;
-      spmm_simt_f32_kernel<<<(unsigned)p->n_simt, SIMT_COLS, 0, st>>>(
-          s, static_cast<const float*>(p->v.tiles), p->v.dp, static_cast<const float*>(B), ldb);
+      if (p->b_dtype == RB_F64)
+        spmm_simt_kernel<double><<<(unsigned)p->n_simt, SIMT_COLS, 0, st>>>(
+            s, static_cast<const double*>(p->v.tiles), p->v.dp, static_cast<const double*>(B), ldb,
+            reinterpret_cast<double*>(C));
+      else
+        spmm_simt_kernel<float><<<(unsigned)p->n_simt, SIMT_COLS, 0, st>>>(
+            s, static_cast<const float*>(p->v.tiles), p->v.dp, static_cast<const float*>(B), ldb, C);
       RB_CUDA_TRY(cudaGetLastError());
       return RB_OK;
     });
   CUtensorMap tmB;
   memset(&tmB, 0, sizeof(tmB));
   int sms = kNumSMs;
-  if (p->b_dtype != RB_F32 && (p->n_tall > 0 || p->n_short > 0 || p->n_sw_steps > 0)) {
+  const bool tc = p->b_dtype == RB_BF16 || p->b_dtype == RB_F16;
+  if (tc && (p->n_tall > 0 || p->n_short > 0 || p->n_sw_steps > 0)) {
     if (int rc = ensure_kernel_attributes()) return rc;
     const CUtensorMapDataType dt =
         p->b_dtype == RB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -2050,7 +2080,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
     RB_CUDA_TRY(cudaGetDevice(&dev));
     RB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  if (p->b_dtype != RB_F32 && p->n_tall > 0)
+  if (tc && p->n_tall > 0)
     tasks.push_back([&](cudaStream_t st) {
       if (p->use_sp) {
         SpmmArgs s = a;
@@ -2089,7 +2119,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       RB_CUDA_TRY(cudaGetLastError());
       return (int)RB_OK;
     });
-  if (p->b_dtype != RB_F32 && p->n_short > 0)
+  if (tc && p->n_short > 0)
     tasks.push_back([&](cudaStream_t st) {
       SpmmArgs s = a;
       s.items = p->d_items + 2 * p->n_tall;
@@ -2107,7 +2137,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       RB_CUDA_TRY(cudaGetLastError());
       return (int)RB_OK;
     });
-  if (p->b_dtype != RB_F32 && p->n_sw_steps > 0)
+  if (tc && p->n_sw_steps > 0)
     tasks.push_back([&](cudaStream_t st) {
       SpmmArgs s = a;
       SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp};

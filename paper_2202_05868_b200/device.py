@@ -349,25 +349,28 @@ class DeviceVbr:
 
     def spmm(self, B: torch.Tensor, out: torch.Tensor | None = None, precision: str | None = None,
              shard: int = 0, n_shards: int = 1, stream=None, sparse24: bool | None = None) -> torch.Tensor:
-        """C[n_rows, N] (float32) = A @ B on the device.  B: [n_cols, N] bf16/fp16/fp32 (row stride
-        a multiple of 8 elements for 16-bit types).  ``out`` rows not owned by ``shard`` are untouched."""
+        """C[n_rows, N] = A @ B on the device: float32 for B bf16/fp16/fp32 (row stride a multiple of 8
+        elements for 16-bit types), float64 for B float64 (the fp64 path).  ``out`` rows not owned by
+        ``shard`` are untouched."""
         if B.dim() != 2 or B.shape[0] != self.n_cols:
             raise ValueError(f"dimension mismatch: {self.n_cols} vs {B.shape[0] if B.dim() == 2 else B.shape}")
-        prec = precision or {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}[B.dtype]
+        prec = precision or {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32",
+                             torch.float64: "fp64"}[B.dtype]
         if L.TORCH_DTYPE[L.PRECISION[prec]] != B.dtype:
             raise ValueError(f"B dtype {B.dtype} does not match precision {prec}")
         N = B.shape[1]
         if B.stride(1) != 1:
             raise ValueError("B must be row-major (stride(1) == 1)")
+        cdt = torch.float64 if prec == "fp64" else torch.float32
         if out is None:
-            out = torch.empty((self.n_rows, N), dtype=torch.float32, device=B.device)
-        if out.dtype != torch.float32 or out.shape != (self.n_rows, N) or out.stride(1) != 1:
-            raise ValueError("out must be float32 [n_rows, N], row-major")
+            out = torch.empty((self.n_rows, N), dtype=cdt, device=B.device)
+        if out.dtype != cdt or out.shape != (self.n_rows, N) or out.stride(1) != 1:
+            raise ValueError(f"out must be {cdt} [n_rows, N], row-major")
         if N == 0 or self.n_rows == 0:
             return out
         h = self.plan(N, prec, shard, n_shards, stream, sparse24=sparse24)
-        L.check(L.lib().rb_spmm_execute(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0),
-                                        L.stream_handle(stream)))
+        run = L.lib().rb_spmm_execute_f64 if prec == "fp64" else L.lib().rb_spmm_execute
+        L.check(run(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0), L.stream_handle(stream)))
         return out
 
     # ---------------------------------------------------------------- reference-format views

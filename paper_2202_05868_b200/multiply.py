@@ -23,7 +23,8 @@ __all__ = ["spmm_vbr", "spmm_vbr_many", "spmm_vbr_device", "spmm_csr", "upload_d
 
 
 NONFINITE_B = ("B contains NaN or Inf: the reference propagates them through the dense block payloads "
-               "(multiply.py:89, zeros included), which the GPU path does not reproduce, so it refuses")
+               "(multiply.py:89, zeros included), which the tensor-core / fp32 paths do not reproduce, so "
+               "they refuse; precision='fp64' reproduces the reference's propagation")
 
 
 def upload_dense(B, precision: str, device=None, nonfinite: torch.Tensor | None = None) -> torch.Tensor:
@@ -69,6 +70,9 @@ def spmm_vbr(V, B, threads: int = 1, *, precision: str | None = None) -> DenseMa
     """Block-based product with un-permute (multiply.py:72-97); float64 DenseMatrix result."""
     if V.n_cols != B.n_rows:
         raise ValueError(f"dimension mismatch: {V.n_cols} vs {B.n_rows}")
+    from . import _forkproxy
+    if _forkproxy.in_bad_fork():  # forked pool worker of a CUDA parent: run in a spawned helper
+        return _forkproxy.call("spmm_vbr", V, B, threads, precision=precision)
     prec = precision or config.default_precision()
     dv = device_vbr_of(V)
     N = B.n_cols
@@ -76,6 +80,8 @@ def spmm_vbr(V, B, threads: int = 1, *, precision: str | None = None) -> DenseMa
         return DenseMatrix(V.n_rows, N, np.zeros((V.n_rows, N)))
     bad = torch.zeros(1, dtype=torch.int32, device=L.require_cuda())
     Bd = upload_dense(B, prec, nonfinite=bad)
+    if prec == "fp64":  # float64 end to end; non-finite B propagates as in the reference
+        return DenseMatrix(V.n_rows, N, dv.spmm(Bd, precision=prec).cpu().numpy())
     C32 = dv.spmm(Bd, precision=prec)
     C64 = torch.empty((V.n_rows, N), dtype=torch.float64, device=C32.device)
     L.check(L.lib().rb_widen_f32(L.ptr(C32), V.n_rows, N, N, L.ptr(C64), N, L.stream_handle()))
@@ -110,8 +116,9 @@ class SpmmPipeline:
         self.depth = depth
         self.b64 = [torch.empty((self.K, self.N), dtype=torch.float64, device=dev) for _ in range(depth)]
         self.bk = [torch.empty((self.K, self.ld), dtype=L.TORCH_DTYPE[self.td], device=dev) for _ in range(depth)]
-        self.c32 = [torch.empty((self.M, self.N), dtype=torch.float32, device=dev) for _ in range(depth)]
         self.c64 = [torch.empty((self.M, self.N), dtype=torch.float64, device=dev) for _ in range(depth)]
+        self.c32 = (self.c64 if self.prec == "fp64" else
+                    [torch.empty((self.M, self.N), dtype=torch.float32, device=dev) for _ in range(depth)])
         self.s_in, self.s_comp, self.s_out = (torch.cuda.Stream(dev) for _ in range(3))
         mk = lambda: [torch.cuda.Event() for _ in range(depth)]  # noqa: E731
         self.ev_in, self.ev_comp, self.ev_out = mk(), mk(), mk()
@@ -137,8 +144,9 @@ class SpmmPipeline:
             if self.used[i]:
                 self.s_comp.wait_event(self.ev_out[i])  # C buffers of step k - depth copied out
             self.dv.spmm(self.bk[i][:, :self.N], out=self.c32[i], precision=self.prec, stream=self.s_comp)
-            L.check(lib.rb_widen_f32(L.ptr(self.c32[i]), self.M, self.N, self.N, L.ptr(self.c64[i]), self.N,
-                                     L.stream_handle(self.s_comp)))
+            if self.prec != "fp64":
+                L.check(lib.rb_widen_f32(L.ptr(self.c32[i]), self.M, self.N, self.N, L.ptr(self.c64[i]), self.N,
+                                         L.stream_handle(self.s_comp)))
             self.ev_comp[i].record(self.s_comp)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_comp[i])
@@ -150,9 +158,10 @@ class SpmmPipeline:
         self.s_out.synchronize()
 
     def check_finite(self) -> None:
-        """Raise ValueError if any B converted so far held NaN / Inf (see NONFINITE_B)."""
+        """Raise ValueError if any B converted so far held NaN / Inf (see NONFINITE_B); the fp64
+        path propagates them instead, as the reference does."""
         self.s_in.synchronize()
-        if int(self.nonfinite.item()):
+        if self.prec != "fp64" and int(self.nonfinite.item()):
             raise ValueError(NONFINITE_B)
 
 

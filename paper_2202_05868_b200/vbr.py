@@ -29,6 +29,9 @@ def vbr_from_grouping(A, grouping, partition: ColumnPartition) -> VbrMatrix:
     """Materialise the VBR form of A under the given row grouping (vbr.py:88-125)."""
     if len(grouping.group_of) != A.n_rows or partition.n_cols != A.n_cols:
         raise ValueError("grouping/partition inconsistent with matrix dimensions")
+    from . import _forkproxy
+    if _forkproxy.in_bad_fork():  # forked pool worker of a CUDA parent: run in a spawned helper
+        return _forkproxy.call("vbr_from_grouping", A, grouping, partition)
     dA = _device_csr_for(A, grouping)
     dg = getattr(grouping, "device", None)
     if dg is not None and dg.n_rows == A.n_rows:

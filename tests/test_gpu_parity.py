@@ -720,3 +720,48 @@ def test_spmm_shard_plans_split_hub_rows(precision, world):
     assert err <= 1e-5 * max(1.0, full.abs().max().item())
     ref = torch.from_numpy(A.to_dense() @ Bh).cuda()
     assert ((C.double() - ref).abs().max() <= 1e-4 * max(1.0, ref.abs().max().item())).item()
+
+
+def test_spmm_fp64_golden_small(golden_small):
+    """fp64 path (float64 CUDA-core kernel over the dense payloads): C within 1e-12 (scaled by |A|·|B|)
+    of the reference's float64 C on every golden case with B; empty rows exactly 0."""
+    n = 0
+    for name, case in golden_small.items():
+        B = golden_b(case)
+        if B is None or "C" not in case:
+            continue
+        A, q = csr_of(case), part_of(case)
+        V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), bool(case["use_compression"])), q)
+        C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision="fp64").data
+        ref = case["C"]
+        bound = np.abs(dense_of(case)) @ np.abs(B)  # mixed-sign cases cancel: scale by |A|·|B|
+        assert_close(C, ref, bound, 1e-12, name)
+        empty = np.diff(case["row_ptr"]) == 0
+        assert np.all(C[empty] == 0.0), name
+        n += 1
+    assert n > 100
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_spmm_fp64_propagates_nonfinite_like_the_reference(bad):
+    """With precision="fp64" a NaN / Inf in B propagates exactly as the reference's dense-payload
+    product does (0 * NaN = NaN inside a stored block's segment, 0 * Inf = NaN, Inf of both signs
+    -> NaN), checked against the oracle's numpy restatement of multiply.py:72-97."""
+    import oracle
+
+    case = load_golden("cfg1_full")
+    A, q = csr_of(case), part_of(case)
+    V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+    B = np.random.default_rng(3).random((A.n_cols, 16))
+    B[17, 5] = bad
+    B[900, 3] = -bad if not np.isnan(bad) else bad
+    C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision="fp64").data
+    bp, bc = oracle.vbr_blocks(case["row_ptr"], case["col_idx"], case["boundaries"], case["row_perm"],
+                               case["row_partition"])
+    pay = oracle.vbr_payloads(case["row_ptr"], case["col_idx"], case["values"], case["boundaries"],
+                              case["row_perm"], case["row_partition"], bp, bc)
+    ref = oracle.spmm_vbr_np(pay, case["row_perm"], case["row_partition"], case["boundaries"], B)
+    assert np.array_equal(np.isnan(C), np.isnan(ref))
+    assert np.array_equal(np.isposinf(C), np.isposinf(ref)) and np.array_equal(np.isneginf(C), np.isneginf(ref))
+    fin = np.isfinite(ref)
+    assert np.isnan(ref).any() and np.allclose(C[fin], ref[fin], rtol=1e-12, atol=0)
