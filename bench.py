@@ -55,6 +55,8 @@ def dist_setup(args):
 
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         if torch.cuda.is_available():
+            if os.environ.get("RB_BENCH_SHARE_GPU"):  # functional test of the N > 1 path on one GPU
+                local, backend = local % torch.cuda.device_count(), "gloo"
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
@@ -255,7 +257,11 @@ def cpu_baseline(args, target_seconds, threads):
 # ---------------------------------------------------------------------------------------- main
 
 
-def build_workload(args, device):
+def build_workload(args, device, world=1, rank=0):
+    """Synthetic config on the device, 1-SA, VBR.  With world > 1 every rank runs the (deterministic)
+    1-SA redundantly and builds only its own shard's VBR (dist.shard_vbr: the rows of its
+    work-balanced range of block rows as a sub-matrix with its own tiles)."""
+    from paper_2202_05868_b200 import dist as rbdist
     from paper_2202_05868_b200 import synth
     from paper_2202_05868_b200.device import DeviceVbr, block_1sa_device
     from paper_2202_05868_b200.types import MergePolicy
@@ -268,12 +274,20 @@ def build_workload(args, device):
     dg = block_1sa_device(dA, bounds, pol, True)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    dv = DeviceVbr.build(dA, bounds, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], dtypes=(cfg.precision,))
+    shard = None
+    if world == 1:
+        dv = DeviceVbr.build(dA, bounds, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], dtypes=(cfg.precision,))
+    else:
+        dv, rows, ranges = rbdist.shard_vbr(dA, bounds, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], cfg.precision,
+                                            rank, world)
+        shard = {"rows": rows, "ranges": ranges, "row_perm": dg.row_perm[: dA.n_rows].to(torch.int64)}
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     stages = {"synth_s": round(t1 - t0, 3), "block_1sa_s": round(t2 - t1, 4), "vbr_build_s": round(t3 - t2, 4),
               "n_groups": dg.n_groups, "n_blocks": dv.n_blocks}
-    return dA, bounds, cfg, meta, dv, stages
+    if shard:
+        stages["shard_rows"] = list(shard["rows"])
+    return dA, bounds, cfg, meta, dv, stages, shard
 
 
 def run_ours(args, world, rank):
@@ -281,17 +295,17 @@ def run_ours(args, world, rank):
     from paper_2202_05868_b200 import synth
 
     device = torch.device("cuda", torch.cuda.current_device())
-    dA, bounds, cfg, meta, dv, stages = build_workload(args, device)
+    dA, bounds, cfg, meta, dv, stages, shard = build_workload(args, device, world, rank)
     prec = cfg.precision
     B = synth.make_b(cfg, dA.n_cols, prec, device=device)
     N = cfg.N
-    C = torch.empty((dA.n_rows, N), dtype=torch.float32, device=device)
-    info = dv.plan_info(N, prec, rank, world)
+    C = torch.empty((dv.n_rows, N), dtype=torch.float32, device=device)  # this rank's rows (all at N=1)
+    info = dv.plan_info(N, prec)
     launches_per_step = int(info["n_launches"])
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        dv.spmm(B, out=C, precision=prec, shard=rank, n_shards=world)
+        dv.spmm(B, out=C, precision=prec)
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -302,7 +316,7 @@ def run_ours(args, world, rank):
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             starts[k].record(stream)
-            dv.spmm(B, out=C, precision=prec, shard=rank, n_shards=world)
+            dv.spmm(B, out=C, precision=prec)
             ends[k].record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -311,12 +325,15 @@ def run_ours(args, world, rank):
     useful = 2.0 * dA.nnz * N
     value = useful / (ms * 1e-3) / 1e9
 
+    gather = run_gather(args, dv, B, C, prec, shard, world, flush, useful) if world > 1 else None
+
     # ---- end to end through the reference-facing path: pinned float64 B -> device -> kernel -> float64 C
     e2e = run_e2e(args, dv, dA, B, prec, rank, world)
     csr = run_csr_comparator(args, dA, B, prec, flush) if world == 1 else None
 
     peaks = measured_peaks()
-    achieved_tflops = useful / (ms_local * 1e-3) / 1e12 if world == 1 else useful / (ms * 1e-3) / 1e12
+    useful_local = 2.0 * dv.csr.nnz * N  # this rank's kernel work (all of it at N=1)
+    achieved_tflops = useful_local / (ms_local * 1e-3) / 1e12
     exec_tflops = info["executed_flops"] / (ms_local * 1e-3) / 1e12
     tensor_dominant = prec != "fp32" and info["core_vbr_flops"] < 0.5 * info["vbr_flops"]
     if tensor_dominant:
@@ -333,9 +350,8 @@ def run_ours(args, world, rank):
         # CUDA-core (skinny / fp32) kernels gather B rows: HBM roofline on the minimal traffic of the
         # product — A read once (nnz x (value + 4 B column)), B read once, C written once (fp32).
         esz = 4 if prec == "fp32" else 2
-        alg_bytes = dA.nnz * (esz + 4) + dA.n_cols * N * esz + dA.n_rows * N * 4
-        ms_ach = ms_local if world == 1 else ms
-        achieved_gbs = alg_bytes / (ms_ach * 1e-3) / 1e9
+        alg_bytes = dv.csr.nnz * (esz + 4) + dA.n_cols * N * esz + dv.n_rows * N * 4
+        achieved_gbs = alg_bytes / (ms_local * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": "spmm_skinny_staged_kernel (h<=4 classes)" if prec != "fp32"
                 else "spmm_skinny*_kernel<float> + spmm_simt_f32_kernel",
                 "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -350,17 +366,44 @@ def run_ours(args, world, rank):
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
         "config": workload_config(cfg, dA.n_rows, dA.n_cols, dA.nnz, world),
-        "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "gather": gather,
         "csr_comparator": csr,
         "clocks": sampler.summary(),
         "stages": dict(stages, rho_prime=round(dA.nnz / max(dv.stored_area(), 1), 5),
-                       padding_executed_over_useful=round(info["executed_flops"] * world / useful, 3),
-                       padding_vbr_over_useful=round(info["vbr_flops"] * world / useful, 3)),
+                       padding_executed_over_useful=round(info["executed_flops"] / useful_local, 3),
+                       padding_vbr_over_useful=round(info["vbr_flops"] / useful_local, 3)),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def run_gather(args, dv, B, C, prec, shard, world, flush, useful):
+    """N > 1: the optional collective of north_star / SURVEY §8(e) — NCCL all-gather of every rank's
+    C rows plus the un-permute into source row order (dist.gather_c, multiply.py:90) — timed after
+    the SpMM in the same step: SpMM + gather per step, max over ranks."""
+    from paper_2202_05868_b200 import dist as rbdist
+
+    steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        dv.spmm(B, out=C, precision=prec)
+        full = rbdist.gather_c(C, shard["row_perm"], shard["ranges"])
+    torch.cuda.synchronize()
+    barrier(world)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for s, e in ev:
+        flush.zero_()
+        s.record()
+        dv.spmm(B, out=C, precision=prec)
+        full = rbdist.gather_c(C, shard["row_perm"], shard["ranges"])
+        e.record()
+    torch.cuda.synchronize()
+    ms = allreduce_max(sum(s.elapsed_time(e) for s, e in ev) / steps, world)
+    del full
+    return {"ms_per_step": round(ms, 4), "value": round(useful / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "what": "SpMM of the rank's shard + NCCL all-gather of C (fp32) + un-permute to source rows, "
+                    "max over ranks; every rank ends with the full C"}
 
 
 def run_csr_comparator(args, dA, B, prec, flush):
@@ -393,10 +436,8 @@ def run_e2e(args, dv, dA, B, prec, rank, world):
 
     N = B.shape[1]
     B_host = [B.double().cpu().pin_memory() for _ in range(2)]
-    C_host = [pinned_dense(dA.n_rows, N) for _ in range(2)]
-    pipe = SpmmPipeline(dv, N, prec)
-    if world > 1:  # each rank runs its own shard of every product
-        pipe.dv = _ShardView(dv, rank, world)
+    C_host = [pinned_dense(dv.n_rows, N) for _ in range(2)]
+    pipe = SpmmPipeline(dv, N, prec)  # at N > 1: this rank's sub-VBR, so only its C rows come back
     for k in range(4):
         pipe.step(k, B_host[k % 2], C_host[k % 2])
     pipe.synchronize()
@@ -413,21 +454,8 @@ def run_e2e(args, dv, dA, B, prec, rank, world):
             "h2d_bytes_per_step": int(B_host[0].numel() * 8), "d2h_bytes_per_step": int(C_host[0].numel() * 8),
             "steps": args.e2e_steps,
             "path": "SpmmPipeline (spmm_vbr_many): pinned float64 B -> H2D -> rb_convert_f64 -> rb_spmm_execute "
-                    "-> rb_widen_f32 -> D2H float64 C, steps overlapped on 3 streams"}
-
-
-class _ShardView:
-    """DeviceVbr facade that runs only this rank's shard of the plan."""
-
-    def __init__(self, dv, rank, world):
-        self._dv, self._rank, self._world = dv, rank, world
-        self.n_rows, self.n_cols = dv.n_rows, dv.n_cols
-
-    def plan(self, N, precision="bf16", stream=None):
-        return self._dv.plan(N, precision, self._rank, self._world, stream)
-
-    def spmm(self, B, out=None, precision=None, stream=None):
-        return self._dv.spmm(B, out=out, precision=precision, shard=self._rank, n_shards=self._world, stream=stream)
+                    "-> rb_widen_f32 -> D2H float64 C, steps overlapped on 3 streams"
+                    + ("" if world == 1 else "; per rank: the whole B in, its shard's C rows out (no gather)")}
 
 
 def run_reference(args, world, rank):

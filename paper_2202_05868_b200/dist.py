@@ -46,9 +46,14 @@ def gather_c(C_local: torch.Tensor, row_perm: torch.Tensor, ranges, group=None) 
     max_rows = max(e - b for b, e in ranges)
     buf = torch.zeros((max_rows, N), dtype=C_local.dtype, device=C_local.device)
     buf[: C_local.shape[0]] = C_local
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf, group=group)
-    out = torch.cat(parts, 0)
+    if buf.is_cuda and dist.get_backend(group) == "gloo":  # gloo (CPU tests / one shared GPU): stage on host
+        parts = [torch.empty_like(buf, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, buf.cpu(), group=group)
+        out = torch.cat(parts, 0).to(buf.device)
+    else:
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf, group=group)
+        out = torch.cat(parts, 0)
     n_rows = row_perm.numel()
     full = torch.empty((n_rows, N), dtype=C_local.dtype, device=C_local.device)
     perm = row_perm.to(C_local.device)
@@ -56,6 +61,57 @@ def gather_c(C_local: torch.Tensor, row_perm: torch.Tensor, ranges, group=None) 
         if e > b:
             full[perm[b:e]] = out[k * max_rows: k * max_rows + (e - b)]
     return full
+
+
+def shard_grouping(row_perm, row_partition, begin: int, end: int):
+    """The shard [begin, end) of permuted rows as a grouping of its own: (rows, row_partition_local).
+
+    ``rows`` are the source row ids of permuted positions begin..end-1; local row i is permuted
+    position begin + i, so the shard's VBR has the identity row_perm and its C comes out in permuted
+    order (what gather_c takes).  ``row_partition_local`` cuts the range at the global block-row
+    boundaries (a tall block row cut by the shard keeps its rows in one local block row).  Works on
+    numpy or torch inputs."""
+    rp = row_partition if isinstance(row_partition, torch.Tensor) else torch.as_tensor(np.asarray(row_partition))
+    rp = rp.to(torch.int64)
+    inner = rp[(rp > begin) & (rp < end)] - begin
+    cuts = torch.cat([torch.zeros(1, dtype=torch.int64, device=rp.device), inner,
+                      torch.full((1,), end - begin, dtype=torch.int64, device=rp.device)])
+    if end <= begin:
+        cuts = torch.zeros(1, dtype=torch.int64, device=rp.device)
+    perm = row_perm if isinstance(row_perm, torch.Tensor) else torch.as_tensor(np.asarray(row_perm))
+    return perm[begin:end].to(torch.int64), cuts
+
+
+def take_rows(A, rows: torch.Tensor):
+    """CSR of the given source rows (in that order) of a DeviceCsr, on A's device (torch gathers)."""
+    from .device import DeviceCsr
+
+    rows = rows.to(A.row_ptr.device)
+    start = A.row_ptr[rows]
+    cnt = A.row_ptr[rows + 1] - start
+    rp = torch.zeros(rows.numel() + 1, dtype=torch.int64, device=rows.device)
+    torch.cumsum(cnt, 0, out=rp[1:])
+    total = int(rp[-1].item()) if rows.numel() else 0
+    idx = torch.repeat_interleave(start - rp[:-1], cnt, output_size=total) + torch.arange(total, device=rows.device)
+    vals = A.values[idx] if A.values is not None else None
+    return DeviceCsr(rows.numel(), A.n_cols, rp, A.col_idx[idx], vals)
+
+
+def shard_vbr(dA, partition, row_perm, row_partition, precision: str, shard: int, n_shards: int, dp: int = 64):
+    """This rank's own VBR: the rows of its work-balanced shard (rb_spmm_shard_range over the full
+    block structure) as a sub-matrix with its own tiles, so a rank holds 1/n_shards of the tiles
+    (each rank builds only its own tiles).  Returns (DeviceVbr, (begin, end), ranges)."""
+    from .device import DeviceVbr
+
+    full = DeviceVbr.build(dA, partition, row_perm, row_partition, dtypes=())  # structure only, no tiles
+    rp, bp, _ = full.host_structure()
+    ranges = all_ranges(rp, bp, precision, dp, n_shards)
+    b, e = ranges[shard]
+    rows, cuts = shard_grouping(full.row_perm64, rp, b, e)
+    sub = take_rows(dA, rows)
+    dv = DeviceVbr.build(sub, partition, torch.arange(e - b, dtype=torch.int64, device=rows.device), cuts,
+                         dtypes=(precision,))
+    return dv, (b, e), ranges
 
 
 def local_rows(C_full_layout: torch.Tensor, row_perm: torch.Tensor, begin: int, end: int) -> torch.Tensor:

@@ -84,3 +84,63 @@ def test_two_rank_sharded_spmm_gather_matches_single_process(name):
     np.testing.assert_allclose(full, ref, rtol=1e-12, atol=1e-12)
     r = np.random.default_rng(7).standard_normal(B.shape[1])
     np.testing.assert_allclose(full @ r, case["C_dot_r"], rtol=1e-9, atol=1e-9)
+
+
+def _worker_subvbr(rank, world, port, name, q):
+    """bench.py --gpus N's per-rank path: the shard's rows become a sub-matrix (dist.take_rows) with
+    its own grouping (dist.shard_grouping: identity row order, cuts at the global block rows), the
+    rank multiplies only that sub-VBR (here: the oracle on its payloads) and gather_c assembles C."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from conftest import golden_b as gb, load_golden as lg
+        from paper_2202_05868_b200 import dist as rbdist
+        from paper_2202_05868_b200.device import DeviceCsr
+
+        case = lg(name)
+        B = gb(case)
+        rp, bp = case["row_partition"], case["blk_ptr"]
+        ranges = rbdist.all_ranges(rp, bp, "bf16", 64, world)
+        b, e = ranges[rank]
+        rows, cuts = rbdist.shard_grouping(case["row_perm"], rp, b, e)
+        A = DeviceCsr(int(case["n_rows"]), int(case["n_cols"]), torch.from_numpy(case["row_ptr"]),
+                      torch.from_numpy(case["col_idx"]), torch.from_numpy(case["values"]))
+        sub = rbdist.take_rows(A, rows)
+        srp, sci, sval = sub.row_ptr.numpy(), sub.col_idx.numpy(), sub.values.numpy()
+        ident = np.arange(e - b, dtype=np.int64)
+        cuts = cuts.numpy()
+        sbp, sbc = oracle.vbr_blocks(srp, sci, case["boundaries"], ident, cuts)
+        pay = oracle.vbr_payloads(srp, sci, sval, case["boundaries"], ident, cuts, sbp, sbc)
+        C_local = oracle.spmm_vbr_np(pay, ident, cuts, case["boundaries"], B)  # permuted order = local order
+        full = rbdist.gather_c(torch.from_numpy(C_local), torch.from_numpy(case["row_perm"]), ranges)
+        if rank == 0:
+            q.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("cfg1_full", 2), ("cfg5_s32", 2), ("cfg4_s8", 3)])
+def test_sharded_sub_vbr_gather_matches_single_process(name, world):
+    import oracle
+
+    case = load_golden(name)
+    B = golden_b(case)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_subvbr, args=(r, world, port, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pay = oracle.vbr_payloads(case["row_ptr"], case["col_idx"], case["values"], case["boundaries"], case["row_perm"],
+                              case["row_partition"], case["blk_ptr"], case["blk_col"])
+    ref = oracle.spmm_vbr_np(pay, case["row_perm"], case["row_partition"], case["boundaries"], B)
+    np.testing.assert_allclose(full, ref, rtol=1e-12, atol=1e-12)
