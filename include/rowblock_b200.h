@@ -159,6 +159,10 @@ typedef struct rb_spmm_info {
 
 int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t b_dtype, int32_t shard,
                         int32_t n_shards, rb_spmm_plan** plan, void* stream);
+/* As rb_spmm_plan_create; work_shards (>= n_shards) = how many GPUs share the whole product when
+ * `vbr` is itself one rank's sub-matrix (dist.shard_vbr): it sizes the parts that split hub rows. */
+int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t n_dense_cols, int32_t b_dtype, int32_t shard,
+                           int32_t n_shards, int32_t work_shards, rb_spmm_plan** plan, void* stream);
 int rb_spmm_plan_info(const rb_spmm_plan* plan, rb_spmm_info* info);
 int rb_spmm_execute(const rb_spmm_plan* plan, const void* B, int64_t ldb, float* C, int64_t ldc, void* stream);
 /* float64 path (plan made with b_dtype RB_F64 over RB_F64 tiles): C float64.  Every block row runs

@@ -1369,20 +1369,32 @@ static void sweep_schedule(const std::vector<int32_t>& rows, const std::vector<i
                            const std::vector<int32_t>& col_bounds, int64_t n_seg, int ctas, int n_slots, int delay,
                            int dpc, std::vector<int4>& steps, std::vector<int32_t>& step_ptr, std::vector<int4>& done,
                            std::vector<int32_t>& done_ptr) {
-  std::vector<std::vector<int32_t>> mine(ctas);
+  // LPT over (block row, slab) items rather than whole block rows: with few rows per CTA (a rank's
+  // shard at 8 GPUs: 512 block rows for 148 CTAs) whole-row assignment leaves a 4-vs-3-rows
+  // imbalance; items balance to within one item.  Each CTA then walks its items slab by slab.
+  std::vector<std::vector<int2>> mine(ctas);  // (g, slab index)
   {
-    std::vector<int32_t> order(rows);
-    std::stable_sort(order.begin(), order.end(),
+    // slab by slab (longest rows first within a slab) onto one running heap: every CTA gets about
+    // the same work in every slab, so the CTAs leave a slab together and the live B window stays
+    // within one slab, while the totals still balance to one item
+    std::vector<int32_t> by_len(rows);
+    std::stable_sort(by_len.begin(), by_len.end(),
                      [&](int32_t x, int32_t y) { return bp[x + 1] - bp[x] > bp[y + 1] - bp[y]; });
+    std::vector<int2> order;
+    order.reserve(rows.size() * slabs.size());
+    for (int32_t si = 0; si < (int32_t)slabs.size(); ++si)
+      for (int32_t g : by_len) order.push_back(make_int2(g, si));
     using E = std::pair<double, int>;
     std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
     for (int c = 0; c < ctas; ++c) heap.push({0.0, c});
-    for (int32_t g : order) {
+    for (const int2& it : order) {
       E top = heap.top();
       heap.pop();
-      mine[top.second].push_back(g);
-      heap.push({top.first + (bp[g + 1] - bp[g]) * (double)dpc + 2.0, top.second});
+      mine[top.second].push_back(it);
+      heap.push({top.first + (bp[it.x + 1] - bp[it.x]) * (double)dpc + 2.0, top.second});
     }
+    for (auto& m : mine)
+      std::stable_sort(m.begin(), m.end(), [](const int2& x, const int2& y) { return x.y < y.y; });
   }
   steps.clear();
   done.clear();
@@ -1396,8 +1408,7 @@ static void sweep_schedule(const std::vector<int32_t>& rows, const std::vector<i
   };
   for (int c = 0; c < ctas; ++c) {
     std::vector<int2> queue;  // (g, n0)
-    for (int32_t n0 : slabs)
-      for (int32_t g : mine[c]) queue.push_back(make_int2(g, n0));
+    for (const int2& it : mine[c]) queue.push_back(make_int2(it.x, slabs[it.y]));
     size_t qi = 0;
     // A row ends where it started (it wraps around once), so rows that start together also finish
     // together and their drains would queue behind each other while the MMA waits for a slot.  The
@@ -1473,9 +1484,18 @@ static void sweep_schedule(const std::vector<int32_t>& rows, const std::vector<i
   }
 }
 
+extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
+                                      int32_t n_shards, int32_t work_shards, rb_spmm_plan** out, void* stream_);
+
 extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
                                    int32_t n_shards, rb_spmm_plan** out, void* stream_) {
+  return rb_spmm_plan_create_ex(vbr, N, b_dtype, shard, n_shards, n_shards, out, stream_);
+}
+
+extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32_t b_dtype, int32_t shard,
+                                      int32_t n_shards, int32_t work_shards, rb_spmm_plan** out, void* stream_) {
   rb::NvtxRange nvtx_range_("rb_spmm_plan_create");
+  if (work_shards < n_shards) work_shards = n_shards;
   if (!vbr || !out) return fail(RB_EINVAL, "null argument");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const bool tc = (b_dtype == RB_BF16 || b_dtype == RB_F16);
@@ -1579,7 +1599,8 @@ extern "C" int rb_spmm_plan_create(const rb_vbr_device* vbr, int64_t N, int32_t 
       // per block than the average skinny row, so at 4+ ranks their 256-block parts become the
       // critical path (config 3, 8 ranks: 0.76 -> 0.48 ms with 64-block parts).  One GPU keeps 256
       // (smaller parts cost more reduction than they save there).
-      int part_max = n_shards >= 8 ? SKINNY_PART_BLOCKS / 4 : n_shards >= 4 ? SKINNY_PART_BLOCKS / 2 : SKINNY_PART_BLOCKS;
+      int part_max = work_shards >= 8 ? SKINNY_PART_BLOCKS / 4
+                     : work_shards >= 4 ? SKINNY_PART_BLOCKS / 2 : SKINNY_PART_BLOCKS;
       if (const char* e = std::getenv("RB_SKINNY_PART_MAX")) part_max = std::max(1, std::atoi(e));
       part[c] = (int)std::min<int64_t>(part_max, std::max<int64_t>(min_batches * nb_batch, want));
     }

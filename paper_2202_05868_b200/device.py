@@ -317,8 +317,9 @@ class DeviceVbr:
         if key not in self._plans:
             s = self._struct(td)
             h = ctypes.c_void_p(0)
-            L.check(L.lib().rb_spmm_plan_create(ctypes.byref(s), int(N), td, int(shard), int(n_shards),
-                                                ctypes.byref(h), L.stream_handle(stream)))
+            work = max(int(n_shards), int(getattr(self, "work_shards", 1)))  # set by dist.shard_vbr
+            L.check(L.lib().rb_spmm_plan_create_ex(ctypes.byref(s), int(N), td, int(shard), int(n_shards), work,
+                                                   ctypes.byref(h), L.stream_handle(stream)))
             if sp24:
                 try:
                     L.check(L.lib().rb_spmm_plan_attach_sparse24(h, ctypes.byref(self.sparse24(td, stream)),

@@ -111,6 +111,7 @@ def shard_vbr(dA, partition, row_perm, row_partition, precision: str, shard: int
     sub = take_rows(dA, rows)
     dv = DeviceVbr.build(sub, partition, torch.arange(e - b, dtype=torch.int64, device=rows.device), cuts,
                          dtypes=(precision,))
+    dv.work_shards = n_shards  # plans size hub-row parts for a 1/n_shards share of the product
     return dv, (b, e), ranges
 
 

@@ -1,7 +1,11 @@
 """Projected multi-GPU scaling on ONE GPU: time every shard's SpMM plan (rb_spmm_plan_create with
 shard k of W, exactly what rank k runs under torchrun) back to back, take the max over shards.
 
-    python tools/shard_sim.py <config> <W,W,...> [steps]
+    python tools/shard_sim.py <config> <W,W,...> [steps] [--plan]
+
+Default: each shard is what bench.py --gpus W's rank k now runs — its own sub-VBR (dist.shard_vbr:
+the rows of its work-balanced block-row range with their own tiles).  --plan times the older form,
+shard k of W of one full plan (rb_spmm_plan_create(shard, n_shards)).
 
 Prints, per W, the max / min shard time and the strong-scaling efficiency t1 / (W * max_k t_k)
 of the sharded compute (B replicated, no collective; the optional C all-gather is separate)."""
@@ -13,7 +17,7 @@ from paper_2202_05868_b200.types import MergePolicy
 
 name = sys.argv[1]
 worlds = [int(x) for x in sys.argv[2].split(',')]
-steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+steps = int(sys.argv[3]) if len(sys.argv) > 3 and not sys.argv[3].startswith("-") else 20
 dA, bounds, cfg, meta = synth.make(name, scale=1, device="cuda")
 dg = block_1sa_device(dA, bounds, MergePolicy(tau=cfg.tau), True)
 dv = DeviceVbr.build(dA, bounds, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], dtypes=(cfg.precision,))
@@ -23,13 +27,20 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
 def time_shard(k, W):
+    if W > 1 and "--plan" not in sys.argv:
+        from paper_2202_05868_b200 import dist as rbdist
+        sub, _, _ = rbdist.shard_vbr(dA, bounds, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], cfg.precision, k, W)
+        Cs = torch.empty((sub.n_rows, cfg.N), dtype=torch.float32, device="cuda")
+        run = lambda: sub.spmm(B, out=Cs, precision=cfg.precision)  # noqa: E731
+    else:
+        run = lambda: dv.spmm(B, out=C, precision=cfg.precision, shard=k, n_shards=W)  # noqa: E731
     for _ in range(3):
-        dv.spmm(B, out=C, precision=cfg.precision, shard=k, n_shards=W)
+        run()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for s, e in ev:
         flush.zero_()
         s.record()
-        dv.spmm(B, out=C, precision=cfg.precision, shard=k, n_shards=W)
+        run()
         e.record()
     torch.cuda.synchronize()
     return sum(s.elapsed_time(e) for s, e in ev) / steps
