@@ -374,7 +374,11 @@ def run_ours(args, world, rank):
                        padding_vbr_over_useful=round(info["vbr_flops"] / useful_local, 3)),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds, os.cpu_count() or 1)
+        if args.config == "3" and args.scale == 1:  # the oracle's 1-SA alone takes minutes at 2^20
+            out["cpu_baseline"] = {"skipped": "config 3's CPU structure (pruned C oracle 1-SA on R-MAT 2^20) takes "
+                                              "~8 min per tau on one core; use --scale 16 for a CPU figure"}
+        else:
+            out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
 

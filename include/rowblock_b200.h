@@ -103,6 +103,16 @@ int rb_vbr_plan(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const in
                 int64_t n_groups, void* workspace, size_t workspace_bytes, int32_t* perm32, int32_t* rpart32,
                 int32_t* blk_ptr, int64_t* grp_tile_row, int32_t* bounds32, int64_t* n_blocks,
                 int64_t* total_tile_rows, void* stream);
+/* Compact payloads of skinny block rows (h <= h_max): cmp_ptr[n_rows+1] (device, int64, by permuted
+ * row: counts of rows of block rows with h <= h_max, 0 elsewhere, prefix-summed) and *total (HOST);
+ * then per such row its nonzeros as int32 global columns and values rounded to tile_dtype held in
+ * float — a block row's payload in block-column order without the segment padding (vbr.py:113-123).
+ * perm32 / rpart32 are rb_vbr_plan outputs.                                                       */
+int rb_vbr_compact_count(int64_t n_rows, const int64_t* row_ptr, const int32_t* perm32, const int32_t* rpart32,
+                         int64_t n_groups, int32_t h_max, int64_t* cmp_ptr, int64_t* total, void* stream);
+int rb_vbr_compact_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                        const int32_t* perm32, const int64_t* cmp_ptr, int32_t tile_dtype, int32_t* cmp_col,
+                        float* cmp_val, void* stream);
 int rb_vbr_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
                 const int64_t* boundaries, int64_t n_seg, int64_t n_groups, void* workspace, size_t workspace_bytes,
                 const int32_t* perm32, const int32_t* rpart32, const int32_t* blk_ptr, const int64_t* grp_tile_row,
@@ -139,6 +149,12 @@ typedef struct rb_vbr_device {
   const int64_t* grp_tile_row;   /* [H] */
   const int32_t* col_bounds;     /* [n_seg+1] */
   const void* tiles;             /* [total_tile_rows x dp] */
+  /* optional compact payloads of skinny block rows (rb_vbr_compact_*; NULL = none): block rows of
+   * h <= cmp_h rows are multiplied from these instead of their tiles */
+  const int64_t* cmp_ptr;        /* [n_rows+1] by permuted row */
+  const int32_t* cmp_col;        /* [cmp_ptr[n_rows]] global columns */
+  const float* cmp_val;          /* values rounded to tile_dtype */
+  int32_t cmp_h;
 } rb_vbr_device;
 
 typedef struct rb_spmm_plan rb_spmm_plan;

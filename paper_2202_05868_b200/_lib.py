@@ -35,7 +35,7 @@ class VbrDevice(ctypes.Structure):
         ("n_rows", I64), ("n_cols", I64), ("n_block_rows", I64), ("n_blocks", I64), ("n_seg", I64),
         ("total_tile_rows", I64), ("dp", I32), ("tile_dtype", I32),
         ("row_partition", P), ("row_perm", P), ("blk_ptr", P), ("blk_col", P), ("grp_tile_row", P),
-        ("col_bounds", P), ("tiles", P),
+        ("col_bounds", P), ("tiles", P), ("cmp_ptr", P), ("cmp_col", P), ("cmp_val", P), ("cmp_h", I32),
     ]
 
 
@@ -73,6 +73,8 @@ def lib():
         L.rb_vbr_plan.argtypes = [I64, I64, P, P, P, I64, P, P, I64, P, SZ, P, P, P, P, P,
                                   ctypes.POINTER(I64), ctypes.POINTER(I64), P]
         L.rb_vbr_emit.argtypes = [I64, P, P, P, P, I64, I64, P, SZ, P, P, P, P, P, P, I32, I32, I64, P]
+        L.rb_vbr_compact_count.argtypes = [I64, P, P, P, I64, I32, P, ctypes.POINTER(I64), P]
+        L.rb_vbr_compact_emit.argtypes = [I64, P, P, P, P, P, I32, P, P, P]
         L.rb_spmm_plan_create.argtypes = [ctypes.POINTER(VbrDevice), I64, I32, I32, I32, ctypes.POINTER(P), P]
         L.rb_spmm_plan_create_ex.argtypes = [ctypes.POINTER(VbrDevice), I64, I32, I32, I32, I32, ctypes.POINTER(P), P]
         L.rb_spmm_plan_info.argtypes = [P, ctypes.POINTER(SpmmInfo)]
@@ -100,7 +102,7 @@ def lib():
         for name in ("rb_csr_plan_create", "rb_csr_execute", "rb_csr_plan_destroy"):
             getattr(L, name).restype = INT
         for name in ("rb_block_1sa_workspace_size", "rb_block_1sa", "rb_vbr_workspace_size", "rb_vbr_plan",
-                     "rb_vbr_emit", "rb_spmm_plan_create", "rb_spmm_plan_create_ex", "rb_spmm_plan_info", "rb_spmm_execute", "rb_spmm_execute_f64",
+                     "rb_vbr_emit", "rb_vbr_compact_count", "rb_vbr_compact_emit", "rb_spmm_plan_create", "rb_spmm_plan_create_ex", "rb_spmm_plan_info", "rb_spmm_execute", "rb_spmm_execute_f64",
                      "rb_spmm_plan_destroy", "rb_convert_f64", "rb_convert_f64_checked", "rb_widen_f32", "rb_group_stats_workspace_size",
                      "rb_group_stats"):
             getattr(L, name).restype = INT

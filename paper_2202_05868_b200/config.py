@@ -33,3 +33,17 @@ def default_sparse24() -> bool:
 def set_default_sparse24(on: bool) -> None:
     global _SPARSE24
     _SPARSE24 = bool(on)
+
+
+_COMPACT_H = int(os.environ.get("RB_COMPACT_H", "8"))  # all skinny block rows (h <= 4 tensor path, <= 8 fp32)
+
+
+def compact_h() -> int:
+    """Block rows of at most this many rows are multiplied from compact payloads (their nonzeros in
+    block-column order, no segment padding) instead of their tiles; 0 = always the tiles."""
+    return _COMPACT_H
+
+
+def set_compact_h(h: int) -> None:
+    global _COMPACT_H
+    _COMPACT_H = max(0, min(8, int(h)))

@@ -59,6 +59,7 @@ constexpr uint32_t SMEM_SHORT = S_STAGES * S_STAGE + 1024 + 256;
 
 constexpr int SIMT_ROWS = 8;
 constexpr int SIMT_COLS = 128;
+constexpr int CMP_PART_NNZ = 2048;  // nonzeros per part of a split row on the compact-payload path
 
 struct SpmmArgs {
   const int32_t* row_partition;
@@ -1236,6 +1237,9 @@ struct rb_spmm_plan {
   int32_t* d_skinny_cnt = nullptr;
   unsigned long long* d_sched = nullptr;  // 2 work counters per skinny height class
   int64_t skinny_off[rb::SKINNY_CLASSES + 1] = {0, 0, 0, 0, 0};
+  rb::SkinnyItem* d_cmp_items = nullptr;  // compact-payload rows (CSR engine over permuted rows)
+  int64_t n_cmp_items = 0;
+  unsigned long long* d_cmp_sched = nullptr;
   CUtensorMap tmA16, tmA32, tmA64, tmA128;
   // multi-slot sweep (spmm_sweep_kernel) for the dominant short height class
   int4* d_sw_steps = nullptr;
@@ -1543,6 +1547,17 @@ extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32
   int64_t sk_slots = 0, sk_units = 0;
   std::vector<int32_t> short_rows;
   std::vector<int2> skinny_rows;  // (g, nb), turned into items once the class totals are known
+  // compact payloads (rb_vbr_compact_*): skinny block rows of h <= cmp_h are multiplied from their
+  // nonzeros (CSR engine over permuted rows) rather than from their padded tiles
+  const bool use_cmp = vbr->cmp_ptr && vbr->cmp_col && vbr->cmp_val && vbr->cmp_h > 0 && b_dtype != RB_F64;
+  std::vector<int64_t> cmp;
+  if (use_cmp) {
+    cmp.resize(vbr->n_rows + 1);
+    RB_CUDA_TRY(cudaMemcpyAsync(cmp.data(), vbr->cmp_ptr, sizeof(int64_t) * (vbr->n_rows + 1),
+                                cudaMemcpyDeviceToHost, stream));
+    RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  std::vector<SkinnyItem> cmp_items;
   for (int64_t g = 0; g < H; ++g) {
     const int h = rp[g + 1] - rp[g];
     const int nb = bp[g + 1] - bp[g];
@@ -1552,7 +1567,31 @@ extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32
         zero_rows.push_back((int32_t)i);
       continue;
     }
-    if (h <= skinny_h) {
+    if (h <= skinny_h && use_cmp && h <= vbr->cmp_h) {
+      // one CSR item per row and C-column slab; hub rows split into CSR_PART_NNZ parts reduced in
+      // part order by the last-arriving part (same workspace as the skinny split rows)
+      for (int64_t pos = std::max<int64_t>(rp[g], row_lo); pos < std::min<int64_t>(rp[g + 1], row_hi); ++pos) {
+        const int64_t nz = cmp[pos + 1] - cmp[pos];
+        if (nz <= 0) continue;  // an empty row inside a non-empty block row: written below as zeros
+        const int nparts = nz > CMP_PART_NNZ ? (int)((nz + CMP_PART_NNZ - 1) / CMP_PART_NNZ) : 1;
+        for (int64_t n0 = 0; n0 < N; n0 += sk_cols) {
+          if (nparts == 1) {
+            cmp_items.push_back(SkinnyItem{(int32_t)pos, (int32_t)n0, 0, (int32_t)nz, 0, 1, -1, 0});
+            continue;
+          }
+          const int32_t slot = (int32_t)sk_slots++, wsoff = (int32_t)sk_units;
+          sk_units += (int64_t)nparts * (sk_cols / 128);
+          for (int q = 0; q < nparts; ++q)
+            cmp_items.push_back(SkinnyItem{(int32_t)pos, (int32_t)n0, (int32_t)(nz * q / nparts),
+                                           (int32_t)(nz * (q + 1) / nparts), q, nparts, slot, wsoff});
+        }
+      }
+      for (int64_t pos = std::max<int64_t>(rp[g], row_lo); pos < std::min<int64_t>(rp[g + 1], row_hi); ++pos)
+        if (cmp[pos + 1] == cmp[pos]) zero_rows.push_back((int32_t)pos);
+      exec_flops += 2.0 * (double)(cmp[rp[g + 1]] - cmp[rp[g]]) * N;
+      vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
+      core_vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
+    } else if (h <= skinny_h) {
       skinny_rows.push_back(make_int2((int)g, nb));
       exec_flops += 2.0 * nb * h * (double)vbr->dp * N;
       vbr_flops += 2.0 * nb * h * (double)vbr->dp * N;
@@ -1690,15 +1729,38 @@ extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32
     cudaError_t e = cudaMalloc(&p->d_skinny, sizeof(SkinnyItem) * all.size());
     if (e == cudaSuccess) e = cudaMalloc(&p->d_sched, sizeof(unsigned long long) * 2 * SKINNY_CLASSES);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->d_sched, 0, sizeof(unsigned long long) * 2 * SKINNY_CLASSES, stream);
-    if (e == cudaSuccess && sk_slots > 0) e = cudaMalloc(&p->d_skinny_ws, sizeof(float) * 128 * (size_t)sk_units);
-    if (e == cudaSuccess && sk_slots > 0) e = cudaMalloc(&p->d_skinny_cnt, sizeof(int32_t) * (size_t)sk_slots);
-    if (e == cudaSuccess && sk_slots > 0) e = cudaMemsetAsync(p->d_skinny_cnt, 0, sizeof(int32_t) * sk_slots, stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(p->d_skinny, all.data(), sizeof(SkinnyItem) * all.size(), cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) {
       rb_spmm_plan_destroy(p);
       return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "skinny work list");
+    }
+  }
+  if (!cmp_items.empty()) {  // longest first (items are pulled dynamically)
+    std::stable_sort(cmp_items.begin(), cmp_items.end(),
+                     [](const SkinnyItem& x, const SkinnyItem& y) { return x.be - x.bb > y.be - y.bb; });
+    p->n_cmp_items = (int64_t)cmp_items.size();
+    cudaError_t e = cudaMalloc(&p->d_cmp_items, sizeof(SkinnyItem) * cmp_items.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_cmp_sched, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_cmp_sched, 0, 2 * sizeof(unsigned long long), stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_cmp_items, cmp_items.data(), sizeof(SkinnyItem) * cmp_items.size(),
+                          cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "compact work list");
+    }
+  }
+  if (sk_slots > 0) {  // split-row partials and arrival counters (skinny and compact items)
+    cudaError_t e = cudaMalloc(&p->d_skinny_ws, sizeof(float) * 128 * (size_t)sk_units);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_skinny_cnt, sizeof(int32_t) * (size_t)sk_slots);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_skinny_cnt, 0, sizeof(int32_t) * sk_slots, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      rb_spmm_plan_destroy(p);
+      return fail(e == cudaErrorMemoryAllocation ? RB_ENOMEM : RB_ECUDA, "split-row workspace");
     }
   }
   const int64_t n_items = 2 * p->n_tall + p->n_short + p->n_simt;
@@ -1826,9 +1888,10 @@ extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32
   p->info.n_sweep_steps = p->n_sw_steps;
   p->info.sweep_slots = p->sw_slots;
   p->info.n_items_simt = p->n_simt;
-  p->info.n_items_skinny = p->skinny_off[SKINNY_CLASSES];
+  p->info.n_items_skinny = p->skinny_off[SKINNY_CLASSES] + p->n_cmp_items;
   p->info.core_vbr_flops = core_vbr_flops;
-  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0) + (p->n_sw_steps > 0);
+  p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0) + (p->n_sw_steps > 0) +
+                       (p->n_cmp_items > 0);
   for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   p->info.executed_flops = exec_flops;
   p->info.vbr_flops = vbr_flops;
@@ -1916,7 +1979,7 @@ extern "C" int rb_spmm_plan_attach_sparse24(rb_spmm_plan* p, const rb_sparse24_d
   p->n_res_items = (int64_t)ritems.size();
   p->use_sp = true;
   p->info.n_launches = (p->n_tall > 0) + (p->n_short > 0) + (p->n_simt > 0) + (p->n_zero > 0) +
-                       (p->n_res_items > 0) + (p->n_sw_steps > 0);
+                       (p->n_res_items > 0) + (p->n_sw_steps > 0) + (p->n_cmp_items > 0);
   for (int c = 0; c < SKINNY_CLASSES; ++c) p->info.n_launches += p->skinny_off[c + 1] > p->skinny_off[c];
   return RB_OK;
 }
@@ -1939,6 +2002,8 @@ extern "C" int rb_spmm_plan_destroy(rb_spmm_plan* p) {
   if (p->d_zero) cudaFree(p->d_zero);
   if (p->d_short_ptr) cudaFree(p->d_short_ptr);
   if (p->d_sw_steps) cudaFree(p->d_sw_steps);
+  if (p->d_cmp_items) cudaFree(p->d_cmp_items);
+  if (p->d_cmp_sched) cudaFree(p->d_cmp_sched);
   if (p->d_sw_done) cudaFree(p->d_sw_done);
   if (p->d_sw_step_ptr) cudaFree(p->d_sw_step_ptr);
   if (p->d_sw_done_ptr) cudaFree(p->d_sw_done_ptr);
@@ -2071,6 +2136,14 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       return launch_skinny(kc, p->b_dtype, c, p->d_sched + 2 * c, st);
     });
   }
+  if (p->n_cmp_items > 0)
+    tasks.push_back([&](cudaStream_t st) {
+      SkinnyArgs kc = k;
+      kc.items = p->d_cmp_items;
+      kc.n_items = p->n_cmp_items;
+      const CsrArgs cr{p->v.cmp_ptr, nullptr, nullptr, p->v.cmp_col, p->v.cmp_val};
+      return launch_csr(kc, cr, p->b_dtype, p->d_cmp_sched, st);
+    });
   if ((p->b_dtype == RB_F32 || p->b_dtype == RB_F64) && p->n_simt > 0)
     tasks.push_back([&](cudaStream_t st) {
       SpmmArgs s = a;

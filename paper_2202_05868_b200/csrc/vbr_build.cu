@@ -359,3 +359,102 @@ extern "C" int rb_vbr_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
 }
+
+// ------------------------------------------------------------------------------------------
+// Compact payloads of skinny block rows.  A block row of h <= h_max rows (config 3 / 2b: almost
+// all h = 1) stores tiles that are mostly the zero padding of its blocks' segments: config 3 holds
+// 1.2 nonzeros per 32-wide block.  Beside the tiles, K4 emits the same payload without the padding:
+// for every permuted row p of such a block row, its nonzeros (global column int32, value rounded to
+// the tile dtype and held in a float) in cmp_ptr[p] .. cmp_ptr[p+1] — the block payloads in
+// block-column order, zeros dropped.  The SpMM multiplies these block rows by gathering only those
+// B rows (the CSR engine of spmm_skinny.cu), reading ~8 B of A per nonzero instead of a 16-byte
+// tile row segment per block.
+namespace rb {
+namespace {
+
+__global__ void compact_count_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ perm32,
+                                     const int32_t* __restrict__ rpart32, int64_t H, int32_t h_max,
+                                     int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < H;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t lo = rpart32[g], hi = rpart32[g + 1];
+    const bool take = hi - lo <= h_max;
+    for (int32_t p = lo + lane; p < hi; p += 32) {
+      const int32_t r = perm32[p];
+      cnt[p] = take ? row_ptr[r + 1] - row_ptr[r] : 0;
+    }
+  }
+}
+
+template <typename T>
+__global__ void compact_emit_kernel(const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col_idx,
+                                    const double* __restrict__ values, const int32_t* __restrict__ perm32, int64_t n,
+                                    const int64_t* __restrict__ cmp_ptr, int32_t* __restrict__ cmp_col,
+                                    float* __restrict__ cmp_val) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < n;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t o = cmp_ptr[p], c = cmp_ptr[p + 1] - o;
+    if (c == 0) continue;
+    const int64_t s = row_ptr[perm32[p]];
+    for (int64_t j = lane; j < c; j += 32) {
+      cmp_col[o + j] = (int32_t)col_idx[s + j];
+      cmp_val[o + j] = (float)cvt<T>(values[s + j]);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace rb
+
+extern "C" int rb_vbr_compact_count(int64_t n_rows, const int64_t* row_ptr, const int32_t* perm32,
+                                    const int32_t* rpart32, int64_t n_groups, int32_t h_max, int64_t* cmp_ptr,
+                                    int64_t* total, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_vbr_compact_count");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (n_rows < 0 || n_groups < 0 || !cmp_ptr || !total) return fail(RB_EINVAL, "bad arguments");
+  RB_CUDA_TRY(cudaMemsetAsync(cmp_ptr, 0, sizeof(int64_t) * (n_rows + 1), stream));
+  if (n_rows > 0 && n_groups > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>((n_groups + 7) / 8, 148 * 32);
+    rb::compact_count_kernel<<<grid, 256, 0, stream>>>(row_ptr, perm32, rpart32, n_groups, h_max, cmp_ptr + 1);
+    RB_CUDA_TRY(cudaGetLastError());
+    size_t tb = 0;
+    RB_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, cmp_ptr + 1, cmp_ptr + 1, (int)n_rows, stream));
+    void* tmp = nullptr;
+    RB_CUDA_TRY(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), stream));
+    const cudaError_t e = cub::DeviceScan::InclusiveSum(tmp, tb, cmp_ptr + 1, cmp_ptr + 1, (int)n_rows, stream);
+    RB_CUDA_TRY(cudaFreeAsync(tmp, stream));
+    RB_CUDA_TRY(e);
+  }
+  RB_CUDA_TRY(cudaMemcpyAsync(total, cmp_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  RB_CUDA_TRY(cudaStreamSynchronize(stream));
+  return RB_OK;
+}
+
+extern "C" int rb_vbr_compact_emit(int64_t n_rows, const int64_t* row_ptr, const int64_t* col_idx,
+                                   const double* values, const int32_t* perm32, const int64_t* cmp_ptr,
+                                   int32_t tile_dtype, int32_t* cmp_col, float* cmp_val, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_vbr_compact_emit");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (n_rows < 0 || !cmp_ptr) return fail(RB_EINVAL, "bad arguments");
+  if (n_rows == 0) return RB_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((n_rows + 7) / 8, 148 * 32);
+  switch (tile_dtype) {
+    case RB_BF16:
+      rb::compact_emit_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(row_ptr, col_idx, values, perm32, n_rows,
+                                                                       cmp_ptr, cmp_col, cmp_val);
+      break;
+    case RB_F16:
+      rb::compact_emit_kernel<__half><<<grid, 256, 0, stream>>>(row_ptr, col_idx, values, perm32, n_rows, cmp_ptr,
+                                                                cmp_col, cmp_val);
+      break;
+    case RB_F32:
+      rb::compact_emit_kernel<float><<<grid, 256, 0, stream>>>(row_ptr, col_idx, values, perm32, n_rows, cmp_ptr,
+                                                               cmp_col, cmp_val);
+      break;
+    default: return fail(RB_EINVAL, "compact payloads need a bf16 / f16 / f32 tile dtype");
+  }
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}

@@ -254,12 +254,44 @@ class DeviceVbr:
         return self.tiles[td]
 
     # ---------------------------------------------------------------- SpMM (rb_spmm_*)
+    def compact(self, td: int, h_max: int, stream=None):
+        """Compact payloads of the block rows with h <= h_max (rb_vbr_compact_*), per tile dtype:
+        (cmp_ptr int64[n_rows+1], cmp_col int32, cmp_val float32) or None if no row qualifies."""
+        cache = self.__dict__.setdefault("_compact", {})
+        key = (td, h_max)
+        if key not in cache:
+            lib = L.lib()
+            dev = self.blk_ptr.device
+            ptr = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
+            total = ctypes.c_int64(0)
+            L.check(lib.rb_vbr_compact_count(self.n_rows, L.ptr(self.csr.row_ptr), L.ptr(self.row_perm),
+                                             L.ptr(self.row_partition), self.n_block_rows, int(h_max), L.ptr(ptr),
+                                             ctypes.byref(total), L.stream_handle(stream)))
+            if total.value == 0:
+                cache[key] = None
+            else:
+                col = torch.empty(total.value, dtype=torch.int32, device=dev)
+                val = torch.empty(total.value, dtype=torch.float32, device=dev)
+                L.check(lib.rb_vbr_compact_emit(self.n_rows, L.ptr(self.csr.row_ptr), L.ptr(self.csr.col_idx),
+                                                L.ptr(self.csr.values), L.ptr(self.row_perm), L.ptr(ptr), td,
+                                                L.ptr(col), L.ptr(val), L.stream_handle(stream)))
+                cache[key] = (ptr, col, val)
+        return cache[key]
+
     def _struct(self, td: int) -> L.VbrDevice:
+        from . import config
+
         t, dp = self.tiles_for(td)
-        return L.VbrDevice(self.n_rows, self.n_cols, self.n_block_rows, self.n_blocks, self.n_seg,
-                           self.total_tile_rows, dp, td, self.row_partition.data_ptr(), self.row_perm.data_ptr(),
-                           self.blk_ptr.data_ptr(), self.blk_col.data_ptr(), self.grp_tile_row.data_ptr(),
-                           self.col_bounds.data_ptr(), t.data_ptr())
+        s = L.VbrDevice(self.n_rows, self.n_cols, self.n_block_rows, self.n_blocks, self.n_seg,
+                        self.total_tile_rows, dp, td, self.row_partition.data_ptr(), self.row_perm.data_ptr(),
+                        self.blk_ptr.data_ptr(), self.blk_col.data_ptr(), self.grp_tile_row.data_ptr(),
+                        self.col_bounds.data_ptr(), t.data_ptr())
+        h_max = config.compact_h()
+        if h_max > 0 and td in (L.RB_BF16, L.RB_F16, L.RB_F32) and self.csr.values is not None:
+            c = self.compact(td, h_max)
+            if c is not None:
+                s.cmp_ptr, s.cmp_col, s.cmp_val, s.cmp_h = c[0].data_ptr(), c[1].data_ptr(), c[2].data_ptr(), h_max
+        return s
 
     # ---------------------------------------------------------------- 2:4 sparse form (rb_sparse24_*)
     def sparse24(self, precision="bf16", stream=None) -> "L.Sparse24Device":
@@ -313,7 +345,7 @@ class DeviceVbr:
 
         td = L.PRECISION[precision] if isinstance(precision, str) else int(precision)
         sp24 = (config.default_sparse24() if sparse24 is None else bool(sparse24)) and td in (L.RB_BF16, L.RB_F16)
-        key = (int(N), td, int(shard), int(n_shards), sp24)
+        key = (int(N), td, int(shard), int(n_shards), sp24, config.compact_h())
         if key not in self._plans:
             s = self._struct(td)
             h = ctypes.c_void_p(0)
