@@ -9,6 +9,7 @@
 // c_fmt [4,6), a_fmt [7,10), b_fmt [10,13), a_major 15, b_major 16,
 // N>>3 [17,23), M>>4 [24,29)).
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda.h>
 
@@ -32,6 +33,21 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef RB_HANG_DEBUG  // developer builds: a wait that never completes reports itself and traps
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                 : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    if (ok) return;
+    if (it == (1ll << 22)) {
+      printf("HANG block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x, addr & 0x3ffff, parity);
+      asm volatile("trap;");
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -44,6 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {

@@ -784,6 +784,15 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 constexpr int MAX_SLOTS = 16;
+// MMA-issuing warps (slots alternate between them).  Two issuers were meant to hide one issuer's
+// per-stage wait + commit (~100+ cycles against an M=128 N=64 MMA of ~48): with 2-stage rings each
+// they measured 2.69 ms against 2.34 ms for one issuer with the 4-stage ring on config 5, so one.
+constexpr int SW_MMA_WARPS = 1;
+constexpr int SW_THREADS = (1 + SW_MMA_WARPS + 4) * 32;
+// Each MMA warp has its own ring of S_STAGES / SW_MMA_WARPS stages (one consumer per ring): with a
+// shared ring a warp that skips the other's steps can run two phases ahead of a stage's barrier,
+// where a parity wait no longer tells the phases apart (it deadlocked).
+constexpr int SW_RING = S_STAGES / SW_MMA_WARPS;
 constexpr uint32_t SMEM_SWEEP = S_STAGES * S_STAGE + 1024 + 512;
 
 struct SweepArgs {
@@ -794,7 +803,7 @@ struct SweepArgs {
   int32_t hp;
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(SW_THREADS, 1)
     spmm_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SpmmArgs a,
                       SweepArgs w) {
   extern __shared__ uint8_t smem_raw[];
@@ -836,38 +845,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch_desc(&tmA);
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_b = policy_evict_last();
-    PipeState ps;
+    PipeState rings[SW_MMA_WARPS];
     int4 nxt = s_begin < s_end ? w.steps[s_begin] : make_int4(0, 0, 0, 0);
     for (int i = s_begin; i < s_end; ++i) {
       int4 st = nxt;
       if (i + 1 < s_end) nxt = w.steps[i + 1];
       const int row0 = __shfl_sync(0xffffffffu, st.x, 0), krow0 = __shfl_sync(0xffffffffu, st.y, 0);
-      const int n0 = __shfl_sync(0xffffffffu, st.z, 0);
+      const int n0 = __shfl_sync(0xffffffffu, st.z, 0), fl = __shfl_sync(0xffffffffu, st.w, 0);
+      const int r = (fl & 0xff) % SW_MMA_WARPS;  // the ring of the MMA warp that owns the step's slot
       const int n_boxes = min(a.short_ns / 64, (a.N - n0 + 63) / 64);
       const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
       for (int kc = 0; kc < a.dp_chunks; ++kc) {
+        const int sg = r * SW_RING + rings[r].s;
         if (elect_one()) {
-          mbar_wait(&empty[ps.s], ps.ph ^ 1);
+          mbar_wait(&empty[sg], rings[r].ph ^ 1);
 #ifdef RB_DBG_NOLOAD  // developer experiment: MMA + barrier pipeline without any operand traffic
-          mbar_arrive(&full[ps.s]);
+          mbar_arrive(&full[sg]);
 #else
-          mbar_arrive_expect_tx(&full[ps.s], tx);
-          uint8_t* sA = smem + ps.s * S_STAGE;
+          mbar_arrive_expect_tx(&full[sg], tx);
+          uint8_t* sA = smem + sg * S_STAGE;
           uint8_t* sB = sA + S_A_SLOT;
-          tma_load_2d_hint(sA, &tmA, &full[ps.s], kc * KCH, row0, pol_a);
+          tma_load_2d_hint(sA, &tmA, &full[sg], kc * KCH, row0, pol_a);
           for (int bx = 0; bx < n_boxes; ++bx)
-            tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[ps.s], n0 + 64 * bx, krow0 + kc * KCH, pol_b);
+            tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[sg], n0 + 64 * bx, krow0 + kc * KCH, pol_b);
 #endif
         }
         __syncwarp();
-        ps.advance(S_STAGES);
+        rings[r].advance(SW_RING);
       }
     }
-    for (int k = 0; k < S_STAGES; ++k) {
-      mbar_wait(&empty[ps.s], ps.ph ^ 1);
-      ps.advance(S_STAGES);
-    }
-  } else if (warp == 1) {
+    for (int r = 0; r < SW_MMA_WARPS; ++r)
+      for (int k = 0; k < SW_RING; ++k) {
+        mbar_wait(&empty[r * SW_RING + rings[r].s], rings[r].ph ^ 1);
+        rings[r].advance(SW_RING);
+      }
+  } else if (warp <= SW_MMA_WARPS) {
+    const int mw = warp - 1;  // this MMA warp issues the steps of slots with slot % SW_MMA_WARPS == mw
     PipeState ps;
 #ifdef RB_PROF_SWEEP
     long long prof_free = 0, prof_full = 0;
@@ -883,6 +896,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (i + 1 < s_end) nxt = w.steps[i + 1];
       const int n0 = __shfl_sync(0xffffffffu, st.z, 0), fl = __shfl_sync(0xffffffffu, st.w, 0);
       const int slot = fl & 0xff;
+      if (slot % SW_MMA_WARPS != mw) continue;  // the other MMA warp's step (its own ring)
       const bool first = (fl >> 8) & 1, last = (fl >> 9) & 1;
       const int n_mt = min(a.short_ns / 128, (a.N - n0 + 127) / 128);
       if (first) {
@@ -900,12 +914,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kc = 0; kc < a.dp_chunks; ++kc) {
         // descriptors = stage-0 descriptor + (byte offset >> 4): one add per operand (SMEM < 256 KB,
         // so the 14-bit address field never carries)
-        const uint64_t soff = (uint64_t)((ps.s * S_STAGE) >> 4);
+        const int sg = mw * SW_RING + ps.s;  // this warp's ring
+        const uint64_t soff = (uint64_t)((sg * S_STAGE) >> 4);
         if (elect_one()) {  // one lane waits and issues (a SYNCS wait by the whole warp costs more)
 #ifdef RB_PROF_SWEEP
           const long long t1 = clock64();
 #endif
-          mbar_wait(&full[ps.s], ps.ph);
+          mbar_wait(&full[sg], ps.ph);
 #ifdef RB_PROF_SWEEP
           prof_full += clock64() - t1;
 #endif
@@ -923,11 +938,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               umma_f16(d, adesc0 + soff + ((kk * 2048) >> 4), bdesc0 + soff + kk * 2, idesc,
                        !(first && kc == 0 && kk == 0));
           }
-          umma_commit(&empty[ps.s]);
+          umma_commit(&empty[sg]);
           if (last && kc + 1 == a.dp_chunks) umma_commit(&sdone[slot]);
         }
         __syncwarp();
-        ps.advance(S_STAGES);
+        ps.advance(SW_RING);
       }
     }
 #ifdef RB_PROF_SWEEP
@@ -2236,7 +2251,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       SpmmArgs s = a;
       SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp};
       const CUtensorMap& tA = p->sw_hp == 16 ? p->tmA16 : p->sw_hp == 32 ? p->tmA32 : p->sw_hp == 64 ? p->tmA64 : p->tmA128;
-      spmm_sweep_kernel<<<(unsigned)p->sw_ctas, TC_THREADS, SMEM_SWEEP, st>>>(tA, tmB, s, w);
+      spmm_sweep_kernel<<<(unsigned)p->sw_ctas, SW_THREADS, SMEM_SWEEP, st>>>(tA, tmB, s, w);
       RB_CUDA_TRY(cudaGetLastError());
       return (int)RB_OK;
     });
