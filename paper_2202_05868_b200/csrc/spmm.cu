@@ -792,8 +792,11 @@ constexpr int SW_THREADS = (1 + SW_MMA_WARPS + 4) * 32;
 // Each MMA warp has its own ring of S_STAGES / SW_MMA_WARPS stages (one consumer per ring): with a
 // shared ring a warp that skips the other's steps can run two phases ahead of a stage's barrier,
 // where a parity wait no longer tells the phases apart (it deadlocked).
-constexpr int SW_RING = S_STAGES / SW_MMA_WARPS;
-constexpr uint32_t SMEM_SWEEP = S_STAGES * S_STAGE + 1024 + 512;
+// Stage ring: 4 x 48 KB (16 KB of tile rows for hp up to 128 + the 32 KB B panel slab of 256
+// columns), or 5 x 40 KB for hp <= 64 (RB_SWEEP_BIG=0).
+constexpr int SW_STAGES_BIG = 4, SW_STAGES_SMALL = 5;
+constexpr uint32_t SW_ASLOT_BIG = 128 * KCH * 2, SW_ASLOT_SMALL = 64 * KCH * 2;
+constexpr uint32_t sweep_smem(int st, uint32_t aslot) { return st * (aslot + S_B_BYTES) + 1024 + 512; }
 
 struct SweepArgs {
   const int4* steps;        // (A tile row, first B row, n0, slot | first << 8 | last << 9)
@@ -803,21 +806,22 @@ struct SweepArgs {
   int32_t hp;
 };
 
+template <int ST, uint32_t ASLOT>
 __global__ void __launch_bounds__(SW_THREADS, 1)
     spmm_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SpmmArgs a,
                       SweepArgs w) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_STAGES * S_STAGE);
-  uint64_t* empty = full + S_STAGES;
-  uint64_t* sdone = empty + S_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (ASLOT + S_B_BYTES));
+  uint64_t* empty = full + ST;
+  uint64_t* sdone = empty + ST;
   uint64_t* sfree = sdone + MAX_SLOTS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + MAX_SLOTS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hp = w.hp;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S_STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -856,28 +860,28 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       const int n_boxes = min(a.short_ns / 64, (a.N - n0 + 63) / 64);
       const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
       for (int kc = 0; kc < a.dp_chunks; ++kc) {
-        const int sg = r * SW_RING + rings[r].s;
+        const int sg = r * (ST / SW_MMA_WARPS) + rings[r].s;
         if (elect_one()) {
           mbar_wait(&empty[sg], rings[r].ph ^ 1);
 #ifdef RB_DBG_NOLOAD  // developer experiment: MMA + barrier pipeline without any operand traffic
           mbar_arrive(&full[sg]);
 #else
           mbar_arrive_expect_tx(&full[sg], tx);
-          uint8_t* sA = smem + sg * S_STAGE;
-          uint8_t* sB = sA + S_A_SLOT;
+          uint8_t* sA = smem + sg * (ASLOT + S_B_BYTES);
+          uint8_t* sB = sA + ASLOT;
           tma_load_2d_hint(sA, &tmA, &full[sg], kc * KCH, row0, pol_a);
           for (int bx = 0; bx < n_boxes; ++bx)
             tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[sg], n0 + 64 * bx, krow0 + kc * KCH, pol_b);
 #endif
         }
         __syncwarp();
-        rings[r].advance(SW_RING);
+        rings[r].advance((ST / SW_MMA_WARPS));
       }
     }
     for (int r = 0; r < SW_MMA_WARPS; ++r)
-      for (int k = 0; k < SW_RING; ++k) {
-        mbar_wait(&empty[r * SW_RING + rings[r].s], rings[r].ph ^ 1);
-        rings[r].advance(SW_RING);
+      for (int k = 0; k < (ST / SW_MMA_WARPS); ++k) {
+        mbar_wait(&empty[r * (ST / SW_MMA_WARPS) + rings[r].s], rings[r].ph ^ 1);
+        rings[r].advance((ST / SW_MMA_WARPS));
       }
   } else if (warp <= SW_MMA_WARPS) {
     const int mw = warp - 1;  // this MMA warp issues the steps of slots with slot % SW_MMA_WARPS == mw
@@ -888,7 +892,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #endif
     uint32_t use_ph = 0;  // bit s: parity of slot s's next sfree wait (flipped per row)
     const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
-    const uint64_t adesc0 = sdesc_sw128(smem_u32(smem) + S_A_SLOT, BOX_BYTES, 1024);  // B panel (MN-major)
+    const uint64_t adesc0 = sdesc_sw128(smem_u32(smem) + ASLOT, BOX_BYTES, 1024);  // B panel (MN-major)
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem), 16, 1024);                    // tile rows (K-major)
     int4 nxt = s_begin < s_end ? w.steps[s_begin] : make_int4(0, 0, 0, 0);
     for (int i = s_begin; i < s_end; ++i) {
@@ -914,8 +918,8 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       for (int kc = 0; kc < a.dp_chunks; ++kc) {
         // descriptors = stage-0 descriptor + (byte offset >> 4): one add per operand (SMEM < 256 KB,
         // so the 14-bit address field never carries)
-        const int sg = mw * SW_RING + ps.s;  // this warp's ring
-        const uint64_t soff = (uint64_t)((sg * S_STAGE) >> 4);
+        const int sg = mw * (ST / SW_MMA_WARPS) + ps.s;  // this warp's ring
+        const uint64_t soff = (uint64_t)((sg * (ASLOT + S_B_BYTES)) >> 4);
         if (elect_one()) {  // one lane waits and issues (a SYNCS wait by the whole warp costs more)
 #ifdef RB_PROF_SWEEP
           const long long t1 = clock64();
@@ -942,7 +946,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
           if (last && kc + 1 == a.dp_chunks) umma_commit(&sdone[slot]);
         }
         __syncwarp();
-        ps.advance(SW_RING);
+        ps.advance((ST / SW_MMA_WARPS));
       }
     }
 #ifdef RB_PROF_SWEEP
@@ -2047,7 +2051,11 @@ static int ensure_kernel_attributes() {
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
-  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SWEEP));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sweep_smem(SW_STAGES_SMALL, SW_ASLOT_SMALL)));
   if (dev >= 0 && dev < 64) done[dev] = true;
   return RB_OK;
 }
@@ -2251,7 +2259,18 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       SpmmArgs s = a;
       SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp};
       const CUtensorMap& tA = p->sw_hp == 16 ? p->tmA16 : p->sw_hp == 32 ? p->tmA32 : p->sw_hp == 64 ? p->tmA64 : p->tmA128;
-      spmm_sweep_kernel<<<(unsigned)p->sw_ctas, SW_THREADS, SMEM_SWEEP, st>>>(tA, tmB, s, w);
+      // 4 x 48 KB measured 2.26 ms against 2.30 ms for 5 x 40 KB on config 5 (3 runs each): the
+      // ring is not the limit, so the 4-stage layout is the default (RB_SWEEP_BIG=0: the 5-stage one)
+      static const bool big_env = [] {
+        const char* e = std::getenv("RB_SWEEP_BIG");
+        return !(e && e[0] == '0');
+      }();
+      if (p->sw_hp > 64 || big_env)
+        spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG>
+            <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG), st>>>(tA, tmB, s, w);
+      else
+        spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL>
+            <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_SMALL, SW_ASLOT_SMALL), st>>>(tA, tmB, s, w);
       RB_CUDA_TRY(cudaGetLastError());
       return (int)RB_OK;
     });
