@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(128) probe(long long* out, int reps, const uin
   if (threadIdx.x == 0) {
     const uint32_t idesc = idesc_f16(M, N, 1, AMN, BMN);
     if (MODE & 4) mbar_arrive(&bar2);  // completes phase 0: later waits on parity 0 return at once
+    uint32_t ready_next = 1;
     const long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
       const uint32_t st = (MODE & 32) ? (((MODE & 1024) ? (r >> 2) & 1 : (r >> 1) & 3)) * ((MODE & 1024) ? 98304 : 49152) : 0;
@@ -47,11 +48,11 @@ __global__ void __launch_bounds__(128) probe(long long* out, int reps, const uin
         mbar_wait(&bar2, 0);
         if (!(MODE & 128)) tc_fence_after();
       }
-      uint32_t ready = 1;
-      if ((MODE & 512) && (r & 1) == 0)  // non-blocking probe of the next stage, result used next round
+      if ((MODE & 512) && (r & 1) == 0) {  // software-pipelined: use the probe issued one stage earlier
+        if (!ready_next) mbar_wait(&bar2, 0);
         asm volatile("{ .reg .pred P; mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
-                     : "=r"(ready) : "r"(smem_u32(&bar2)), "r"(0u) : "memory");
-      if ((MODE & 512) && !ready) mbar_wait(&bar2, 0);
+                     : "=r"(ready_next) : "r"(smem_u32(&bar2)), "r"(0u));
+      }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         // K-major: rows of 128 B (64 K), +32 B per K16; MN-major: [k][64-wide chunk] boxes of 8 KB, +2 KB per K16
@@ -314,7 +315,8 @@ int main() {
   run<128, 64, 1, 0, 4 + 512>("swap +test_wait per 8", d_out, sms);
   run<128, 64, 1, 0, 63 + 256 + 1024>("swap everything, syncs per 16, desc add", d_out, sms);
   run<128, 64, 1, 0, 5 + 1024>("swap wait+commit per 16", d_out, sms);
-  run<128, 64, 1, 0, 1 + 4 + 512 + 32 + 256 + 128>("swap test_wait+commit+stages(add)", d_out, sms);
+  run<128, 64, 1, 0, 1 + 4 + 512 + 32 + 256 + 128>("swap pipelined test_wait+commit+stages(add)", d_out, sms);
+  run<128, 64, 1, 0, 1 + 4 + 32 + 256 + 128>("swap blocking wait+commit+stages(add)", d_out, sms);
   run<128, 256, 0, 1, 32>("tall-like N=256 +4 stages", d_out, sms);
   run<128, 64, 1, 0, 64>("swap +TMA writes 40KB/8 MMA", d_out, sms);
   run<128, 64, 1, 0, 96>("swap +TMA writes +4 stages", d_out, sms);
