@@ -806,7 +806,9 @@ struct SweepArgs {
   int32_t hp;
 };
 
-template <int ST, uint32_t ASLOT>
+// PAIR: the full barrier of an even stage covers it and the next one (2 arrivals per phase), so the
+// MMA warp waits once per two stages (16 MMAs) instead of once per stage.
+template <int ST, uint32_t ASLOT, bool PAIR>
 __global__ void __launch_bounds__(SW_THREADS, 1)
     spmm_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SpmmArgs a,
                       SweepArgs w) {
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PAIR ? 2 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < MAX_SLOTS; ++s) {
@@ -861,23 +863,30 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
       for (int kc = 0; kc < a.dp_chunks; ++kc) {
         const int sg = r * (ST / SW_MMA_WARPS) + rings[r].s;
+        uint64_t* fb = &full[PAIR ? (sg & ~1) : sg];
         if (elect_one()) {
           mbar_wait(&empty[sg], rings[r].ph ^ 1);
 #ifdef RB_DBG_NOLOAD  // developer experiment: MMA + barrier pipeline without any operand traffic
-          mbar_arrive(&full[sg]);
+          mbar_arrive(fb);
 #else
-          mbar_arrive_expect_tx(&full[sg], tx);
+          mbar_arrive_expect_tx(fb, tx);
           uint8_t* sA = smem + sg * (ASLOT + S_B_BYTES);
           uint8_t* sB = sA + ASLOT;
-          tma_load_2d_hint(sA, &tmA, &full[sg], kc * KCH, row0, pol_a);
+          tma_load_2d_hint(sA, &tmA, fb, kc * KCH, row0, pol_a);
           for (int bx = 0; bx < n_boxes; ++bx)
-            tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, &full[sg], n0 + 64 * bx, krow0 + kc * KCH, pol_b);
+            tma_load_2d_hint(sB + bx * BOX_BYTES, &tmB, fb, n0 + 64 * bx, krow0 + kc * KCH, pol_b);
 #endif
         }
         __syncwarp();
         rings[r].advance((ST / SW_MMA_WARPS));
       }
     }
+    if (PAIR)  // a pair left half-filled: complete its phase (the MMA warp waits on it)
+      for (int r = 0; r < SW_MMA_WARPS; ++r)
+        if (rings[r].s & 1) {
+          if (elect_one()) mbar_arrive(&full[r * (ST / SW_MMA_WARPS) + rings[r].s - 1]);
+          __syncwarp();
+        }
     for (int r = 0; r < SW_MMA_WARPS; ++r)
       for (int k = 0; k < (ST / SW_MMA_WARPS); ++k) {
         mbar_wait(&empty[r * (ST / SW_MMA_WARPS) + rings[r].s], rings[r].ph ^ 1);
@@ -924,7 +933,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #ifdef RB_PROF_SWEEP
           const long long t1 = clock64();
 #endif
-          mbar_wait(&full[sg], ps.ph);
+          if (!PAIR || (sg & 1) == 0) mbar_wait(&full[PAIR ? (sg & ~1) : sg], ps.ph);
 #ifdef RB_PROF_SWEEP
           prof_full += clock64() - t1;
 #endif
@@ -2051,9 +2060,11 @@ static int ensure_kernel_attributes() {
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TALL));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SHORT));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
-  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG>,
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
-  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL>,
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    sweep_smem(SW_STAGES_SMALL, SW_ASLOT_SMALL)));
   if (dev >= 0 && dev < 64) done[dev] = true;
@@ -2265,11 +2276,18 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
         const char* e = std::getenv("RB_SWEEP_BIG");
         return !(e && e[0] == '0');
       }();
-      if (p->sw_hp > 64 || big_env)
-        spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG>
+      static const bool pair_env = [] {
+        const char* e = std::getenv("RB_SWEEP_PAIR");
+        return e && e[0] == '1';
+      }();
+      if (pair_env)
+        spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, true>
+            <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG), st>>>(tA, tmB, s, w);
+      else if (p->sw_hp > 64 || big_env)
+        spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false>
             <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG), st>>>(tA, tmB, s, w);
       else
-        spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL>
+        spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL, false>
             <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_SMALL, SW_ASLOT_SMALL), st>>>(tA, tmB, s, w);
       RB_CUDA_TRY(cudaGetLastError());
       return (int)RB_OK;

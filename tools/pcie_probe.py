@@ -1,7 +1,8 @@
 """Host<->device copy bandwidth on the box: H2D, D2H and both at once (pinned, 134 MB each),
 the bound of bench.py's e2e (config 2 moves 134 MB of float64 B in and 134 MB of C out per step)."""
 import torch
-n = 32768 * 512
+import sys
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768 * 512
 h_in = torch.empty(n, dtype=torch.float64).pin_memory()
 h_out = torch.empty(n, dtype=torch.float64).pin_memory()
 d_in = torch.empty(n, dtype=torch.float64, device="cuda")
