@@ -257,6 +257,94 @@ def test_spmm_sweep_kernel(h, delta, N, delay, monkeypatch):
     assert np.array_equal(C, C2)
 
 
+@pytest.mark.parametrize("variant", [("RB_SWEEP_PAIR", "1"), ("RB_SWEEP_BIG", "0"), ("RB_SWEEP_DELAY", "20")])
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+def test_spmm_sweep_kernel_variants(variant, precision, monkeypatch):
+    """The sweep kernel's stage-ring variants (pair barriers, 5 x 40 KB ring, long slot delay) and
+    fp16 operands on config 5's shape (h = 64, N = 1024 -> 4 slabs), forced on a small matrix."""
+    monkeypatch.setenv("RB_SWEEP", "2")
+    monkeypatch.setenv(*variant)
+    rng = np.random.default_rng(hash(variant) % 1000)
+    n_groups, h, delta, n_seg, N = 160, 64, 64, 40, 1024
+    from paper_2202_05868_b200.types import RowGroup, RowGrouping, csr_from_coo
+    rows, cols = [], []
+    for gi in range(n_groups):
+        for sgi in rng.choice(n_seg, size=int(rng.integers(1, 8)), replace=False):
+            for r in range(gi * h, (gi + 1) * h):
+                c = rng.choice(np.arange(sgi * delta, (sgi + 1) * delta), size=int(rng.integers(1, 6)), replace=False)
+                rows.append(np.full(len(c), r))
+                cols.append(c)
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    tdt = torch.float16 if precision == "fp16" else torch.bfloat16
+    vals = rounded(rng.uniform(-1, 1, len(rows)), tdt)
+    keep = vals != 0
+    A = csr_from_coo(n_groups * h, n_seg * delta, rows[keep], cols[keep], vals[keep], sum_duplicates=True)
+    go = np.repeat(np.arange(n_groups), h)
+    G = RowGrouping(go, [RowGroup(np.arange(g * h, (g + 1) * h), np.zeros(0), 0) for g in range(n_groups)])
+    V = rb.vbr_from_grouping(A, G, rb.ColumnPartition.uniform(n_seg * delta, delta))
+    B = rounded(rng.uniform(-1, 1, (n_seg * delta, N)), tdt)
+    assert V.device.plan_info(N, precision)["n_sweep_steps"] > 0
+    C = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision=precision).data
+    Ad = A.to_dense()
+    assert_close(C, Ad @ B, np.abs(Ad) @ np.abs(B), 1e-4, str(variant))
+
+
+@pytest.mark.parametrize("name", ["rmat12_t3", "rmat16_t7", "cfg1_full"])
+@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp32"])
+def test_compact_payloads_match_tiles(name, precision, monkeypatch):
+    """Skinny block rows multiplied from compact payloads (default) and from their padded tiles
+    (RB_COMPACT_H=0): both within the stated tolerance of the float64 product of the same rounded
+    inputs, the compact run launching the CSR engine and no tile skinny kernel."""
+    import scipy.sparse as sp
+    from paper_2202_05868_b200 import config
+
+    case = load_golden(name)
+    A, q = csr_of(case), part_of(case)
+    B = golden_b(case)
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[precision]
+    Ar = sp.csr_matrix((rounded(A.values, tdt) if precision != "fp32" else A.values.astype(np.float32).astype(np.float64),
+                        A.col_idx, A.row_ptr), shape=(A.n_rows, A.n_cols))
+    Br = rounded(B, tdt) if precision != "fp32" else B.astype(np.float32).astype(np.float64)
+    ref = Ar @ Br
+    bound = abs(Ar) @ np.abs(Br)
+    out = {}
+    for h in (8, 0):
+        monkeypatch.setattr(config, "_COMPACT_H", h)
+        V = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q)
+        out[h] = rb.spmm_vbr(V, rb.DenseMatrix.from_array(B), precision=precision).data
+        assert_close(out[h], ref, bound, 1e-5 if precision == "fp32" else 1e-4, f"{name} compact_h={h}")
+    empty = np.diff(A.row_ptr) == 0
+    assert np.all(out[8][empty] == 0.0)
+
+
+def test_shard_sub_vbrs_assemble_full_product():
+    """bench.py --gpus N's per-rank path on one GPU: every rank's sub-VBR (dist.shard_vbr, own tiles)
+    computes its rows in permuted order; placed at row_perm they equal the single-GPU product."""
+    from paper_2202_05868_b200 import dist as rbdist
+    from paper_2202_05868_b200.device import DeviceCsr, block_1sa_device
+    from paper_2202_05868_b200.types import MergePolicy
+
+    for name in ("cfg5_s32", "cfg4_s8", "rmat12_t3"):
+        case = load_golden(name)
+        A, q = csr_of(case), part_of(case)
+        dA = DeviceCsr.from_host(A)
+        dg = block_1sa_device(dA, q, MergePolicy(tau=float(case["tau"])), True)
+        B = torch.from_numpy(golden_b(case)).to(torch.bfloat16).cuda()
+        full = rb.vbr_from_grouping(A, rb.block_1sa(A, q, policy_of(case), True), q).device.spmm(B, precision="bf16")
+        perm = dg.row_perm[: A.n_rows].to(torch.int64)
+        for world in (2, 3, 8):
+            C = torch.full_like(full, float("nan"))
+            for k in range(world):
+                dv, (b, e), _ = rbdist.shard_vbr(dA, q, dg.row_perm, dg.group_ptr[: dg.n_groups + 1], "bf16", k, world)
+                assert dv.n_rows == e - b
+                if e > b:
+                    C[perm[b:e]] = dv.spmm(B, precision="bf16")
+            torch.cuda.synchronize()
+            assert not torch.isnan(C).any(), (name, world)
+            err = (C.double() - full.double()).abs().max().item()
+            assert err <= 1e-5 * max(1.0, full.abs().max().item()), (name, world, err)
+
+
 def test_spmm_medium_cfg5_through_sweep(monkeypatch):
     """The reference-generated 1/32-scale config 5 (128 block rows of h = 64) through the sweep kernel."""
     monkeypatch.setenv("RB_SWEEP", "2")
