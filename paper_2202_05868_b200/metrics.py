@@ -9,8 +9,9 @@ Same dataclasses, functions, defaults and errors as the reference:
 
 The per-group reductions (stored columns, element nnz, distinct-segment counts) and the exact
 rational density tests run in one CUDA kernel (csrc/stats.cu, rb_group_stats) on the grouping's
-device arrays; blocking_curve runs 1-SA on the device once per tau, sequentially (the 1-SA kernel
-is a persistent cooperative grid that owns the GPU; ``jobs`` is accepted and ignored).
+device arrays; blocking_curve runs 1-SA on the device once per tau.  The 1-SA kernel is a persistent
+grid that owns its GPU, so with ``jobs != 1`` the points run concurrently across the visible GPUs
+(one host thread per device), and sequentially on any one device.
 """
 
 from __future__ import annotations
@@ -168,20 +169,62 @@ def blocking_stats(A, grouping, partition: ColumnPartition, tau: float | None = 
 
 
 def blocking_curve(A, partition: ColumnPartition, taus, policy: MergePolicy = MergePolicy(),
-                   use_compression: bool = True, jobs: int = 1, meta: dict | None = None) -> BlockingCurve:
-    """1-SA + stats once per tau on the same input (metrics.py:106-130); points ordered by tau."""
+                   use_compression: bool = True, jobs: int = 1, meta: dict | None = None,
+                   devices=None) -> BlockingCurve:
+    """1-SA + stats once per tau on the same input (metrics.py:106-130); points ordered by tau.
+
+    The reference spreads the points over ``jobs`` worker processes (metrics.py:122).  Here every
+    point is one device 1-SA (a grid-wide persistent kernel that occupies a whole GPU), so points run
+    concurrently across GPUs: with ``jobs != 1`` they are dealt round robin to ``devices`` (default:
+    every visible GPU), one host thread per device, each device holding its own copy of A.  Points
+    that share a device run one after another on it.  Results are identical to the sequential run
+    (the 1-SA is deterministic)."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
     taus = [float(t) for t in taus]
     if not taus or any(not 0.0 <= t <= 1.0 for t in taus):
         raise ValueError("taus must be non-empty and within [0, 1]")
     if any(b <= a for a, b in zip(taus, taus[1:])):
         raise ValueError("taus must be strictly increasing")
-    dA = A if isinstance(A, DeviceCsr) else DeviceCsr.from_host(A)
-    points = []
-    for t in taus:
-        p = MergePolicy(similarity=policy.similarity, tau=t, bounded=policy.bounded,
-                        pattern_update=policy.pattern_update)
-        dg = block_1sa_device(dA, partition, p, use_compression)
-        points.append((t, blocking_stats(dA, dg, partition, tau=t, check_bound=policy.bounded)))
+    if devices is None:
+        devices = list(range(torch.cuda.device_count())) if jobs != 1 else [None]
+    devices = list(devices) or [None]
+    src = A if isinstance(A, DeviceCsr) else None
+    copies, locks = {}, {d: threading.Lock() for d in devices}
+
+    def csr_on(d):
+        if d not in copies:
+            if src is not None and (d is None or src.row_ptr.device == torch.device("cuda", d)):
+                copies[d] = src
+            elif src is not None:
+                dev = torch.device("cuda", d)
+                copies[d] = DeviceCsr(src.n_rows, src.n_cols, src.row_ptr.to(dev), src.col_idx.to(dev),
+                                      None if src.values is None else src.values.to(dev))
+            else:
+                copies[d] = DeviceCsr.from_host(A, None if d is None else torch.device("cuda", d))
+        return copies[d]
+
+    def point(k):
+        d = devices[k % len(devices)]
+        with locks[d]:
+            if d is not None:
+                torch.cuda.set_device(d)
+            dA_d = csr_on(d)
+            t = taus[k]
+            p = MergePolicy(similarity=policy.similarity, tau=t, bounded=policy.bounded,
+                            pattern_update=policy.pattern_update)
+            dg = block_1sa_device(dA_d, partition, p, use_compression)
+            return t, blocking_stats(dA_d, dg, partition, tau=t, check_bound=policy.bounded)
+
+    if len(devices) == 1:
+        points = [point(k) for k in range(len(taus))]
+    else:
+        with ThreadPoolExecutor(max_workers=len(devices)) as ex:
+            points = list(ex.map(point, range(len(taus))))
+    dA = csr_on(devices[0])
     base = {"n_rows": dA.n_rows, "n_cols": dA.n_cols, "nnz": dA.nnz}
     if meta:
         base.update(meta)

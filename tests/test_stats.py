@@ -136,6 +136,10 @@ def test_device_curve_matches_reference():
         assert s.rho_prime == float(ref["rho_prime"][i]) and s.delta_h_prime == float(ref["delta_h_prime"][i])
         assert s.density_bound_ok == bool(ref["density_bound_ok"][i])
     assert M.curve_select(curve, at_height=1.2)[0] == float(ref["select_h_1.2"])
+    # the concurrent form (one host thread per listed device; points sharing a device serialise)
+    # gives the same curve; on a 1-GPU box both threads use cuda:0
+    par = M.blocking_curve(A, q, [float(t) for t in ref["taus"]], rb.MergePolicy(tau=0.5), jobs=2, devices=[0, 0])
+    assert par.taus() == curve.taus() and [s for _, s in par.points] == [s for _, s in curve.points]
     with pytest.raises(ValueError):
         M.blocking_curve(A, q, [0.5, 0.3])
     with pytest.raises(ValueError):
