@@ -789,6 +789,16 @@ constexpr int MAX_SLOTS = 16;
 // they measured 2.69 ms against 2.34 ms for one issuer with the 4-stage ring on config 5, so one.
 constexpr int SW_MMA_WARPS = 1;
 constexpr int SW_THREADS = (1 + SW_MMA_WARPS + 4) * 32;
+constexpr int SW64_THREADS = (1 + SW_MMA_WARPS + 8) * 32;  // M64 form: 8 epilogue warps
+#ifdef RB_DBG_NOEPI  // developer experiment: no epilogue (C is not written)
+constexpr bool NOEPI_DBG = true;
+#else
+constexpr bool NOEPI_DBG = false;
+#endif
+// Idle epilogue warps probe their slot barrier with one lane and sleep between probes.
+#ifndef SW_EPI_SLEEP_NS
+#define SW_EPI_SLEEP_NS 256
+#endif
 // Each MMA warp has its own ring of S_STAGES / SW_MMA_WARPS stages (one consumer per ring): with a
 // shared ring a warp that skips the other's steps can run two phases ahead of a stage's barrier,
 // where a parity wait no longer tells the phases apart (it deadlocked).
@@ -797,6 +807,8 @@ constexpr int SW_THREADS = (1 + SW_MMA_WARPS + 4) * 32;
 constexpr int SW_STAGES_BIG = 4, SW_STAGES_SMALL = 5;
 constexpr uint32_t SW_ASLOT_BIG = 128 * KCH * 2, SW_ASLOT_SMALL = 64 * KCH * 2;
 constexpr uint32_t sweep_smem(int st, uint32_t aslot) { return st * (aslot + S_B_BYTES) + 1024 + 512; }
+constexpr uint32_t SW64_EPI_BYTES = 8 * 16 * 36 * 4;  // M64 epilogue staging: 16 x 36 floats per warp
+constexpr uint32_t sweep64_smem() { return SW_STAGES_BIG * (SW_ASLOT_BIG + S_B_BYTES) + 1024 + 1024 + SW64_EPI_BYTES; }
 
 struct SweepArgs {
   const int4* steps;        // (A tile row, first B row, n0, slot | first << 8 | last << 9)
@@ -808,8 +820,45 @@ struct SweepArgs {
 
 // PAIR: the full barrier of an even stage covers it and the next one (2 arrivals per phase), so the
 // MMA warp waits once per two stages (16 MMAs) instead of once per stage.
-template <int ST, uint32_t ASLOT, bool PAIR>
-__global__ void __launch_bounds__(SW_THREADS, 1)
+// Step list reader for the producer / MMA warps: the warp loads 32 steps at a time (one per lane,
+// coalesced) one batch ahead and hands step i to every lane with __shfl_sync.  A per-step load
+// issued one step ahead left its L2/DRAM latency (~1 us under this kernel's memory load) on the
+// issue path of every step.
+struct StepReader {
+  const int4* p;
+  int end, base, lane;
+  int4 cur, nxt;
+  __device__ __forceinline__ int4 load(int idx) const { return idx < end ? __ldg(p + idx) : make_int4(0, 0, 0, 0); }
+  __device__ __forceinline__ void init(const int4* steps, int b, int e, int ln) {
+    p = steps;
+    end = e;
+    base = b;
+    lane = ln;
+    cur = load(b + ln);
+    nxt = load(b + 32 + ln);
+  }
+  __device__ __forceinline__ int4 get(int i) {  // i = base, base + 1, ... in order
+    if (i - base == 32) {
+      base += 32;
+      cur = nxt;
+      nxt = load(base + 32 + lane);
+    }
+    const int k = i - base;
+    return make_int4(__shfl_sync(0xffffffffu, cur.x, k), __shfl_sync(0xffffffffu, cur.y, k),
+                     __shfl_sync(0xffffffffu, cur.z, k), __shfl_sync(0xffffffffu, cur.w, k));
+  }
+};
+
+// M64: block rows of exactly hp = 64 on NON-swapped MMAs, D[64 rows x 256 C columns] =
+// tile[64 x K] (K-major) x Bpanel[K x 256] (MN-major), one tcgen05.mma M=64 N=256 K=16 per K16.  An
+// M=64 accumulator fills one lane half of TMEM (rows 16q..16q+15 at lanes 32q + 16*half + 0..15;
+// tools/mma_probe/m64_layout.cu), so slot s sits at lane half s & 1, columns (s >> 1) * 256: the
+// same 4 slots of 64 rows x 256 columns as the swapped form, with half as many MMAs per block and
+// each one 128 cycles long — the per-stage wait / commit no longer starves the tensor pipe, as the
+// 48-cycle swapped N=64 MMAs did.  Eight epilogue warps (two per lane quadrant, one per 128-column
+// half) each copy 16 rows x 128 columns to registers, release the slot, then store.
+template <int ST, uint32_t ASLOT, bool PAIR, bool M64 = false>
+__global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     spmm_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SpmmArgs a,
                       SweepArgs w) {
   extern __shared__ uint8_t smem_raw[];
@@ -829,7 +878,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     }
     for (int s = 0; s < MAX_SLOTS; ++s) {
       mbar_init(&sdone[s], 1);
-      mbar_init(&sfree[s], 4);
+      mbar_init(&sfree[s], M64 ? 8 : 4);
     }
     fence_mbar_init();
   }
@@ -847,17 +896,21 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   // each step: ~165 cycles per M=128 N=64 MMA against the 48-cycle issue floor measured by
   // tools/mma_probe.)
   if (warp == 0) {
+#ifdef RB_DBG_MMAONLY  // developer experiment: MMA issue loop alone (no producer, no stage barriers)
+    if (true) {
+    } else
+#endif
+    {
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmA);
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_b = policy_evict_last();
     PipeState rings[SW_MMA_WARPS];
-    int4 nxt = s_begin < s_end ? w.steps[s_begin] : make_int4(0, 0, 0, 0);
+    StepReader rd;
+    rd.init(w.steps, s_begin, s_end, lane);
     for (int i = s_begin; i < s_end; ++i) {
-      int4 st = nxt;
-      if (i + 1 < s_end) nxt = w.steps[i + 1];
-      const int row0 = __shfl_sync(0xffffffffu, st.x, 0), krow0 = __shfl_sync(0xffffffffu, st.y, 0);
-      const int n0 = __shfl_sync(0xffffffffu, st.z, 0), fl = __shfl_sync(0xffffffffu, st.w, 0);
+      const int4 st = rd.get(i);
+      const int row0 = st.x, krow0 = st.y, n0 = st.z, fl = st.w;
       const int r = (fl & 0xff) % SW_MMA_WARPS;  // the ring of the MMA warp that owns the step's slot
       const int n_boxes = min(a.short_ns / 64, (a.N - n0 + 63) / 64);
       const uint32_t tx = (uint32_t)hp * KCH * 2 + n_boxes * BOX_BYTES;
@@ -892,6 +945,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         mbar_wait(&empty[r * (ST / SW_MMA_WARPS) + rings[r].s], rings[r].ph ^ 1);
         rings[r].advance((ST / SW_MMA_WARPS));
       }
+    }
   } else if (warp <= SW_MMA_WARPS) {
     const int mw = warp - 1;  // this MMA warp issues the steps of slots with slot % SW_MMA_WARPS == mw
     PipeState ps;
@@ -900,14 +954,15 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     const long long prof_t0 = clock64();
 #endif
     uint32_t use_ph = 0;  // bit s: parity of slot s's next sfree wait (flipped per row)
-    const uint32_t idesc = idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
+    const uint32_t idesc = M64 ? idesc_f16(64, 256, a.ab_fmt, /*a_mn=*/0, /*b_mn=*/1)
+                               : idesc_f16(128, hp, a.ab_fmt, /*a_mn=*/1, /*b_mn=*/0);
     const uint64_t adesc0 = sdesc_sw128(smem_u32(smem) + ASLOT, BOX_BYTES, 1024);  // B panel (MN-major)
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem), 16, 1024);                    // tile rows (K-major)
-    int4 nxt = s_begin < s_end ? w.steps[s_begin] : make_int4(0, 0, 0, 0);
+    StepReader rd;
+    rd.init(w.steps, s_begin, s_end, lane);
     for (int i = s_begin; i < s_end; ++i) {
-      int4 st = nxt;
-      if (i + 1 < s_end) nxt = w.steps[i + 1];
-      const int n0 = __shfl_sync(0xffffffffu, st.z, 0), fl = __shfl_sync(0xffffffffu, st.w, 0);
+      const int4 st = rd.get(i);
+      const int n0 = st.z, fl = st.w;
       const int slot = fl & 0xff;
       if (slot % SW_MMA_WARPS != mw) continue;  // the other MMA warp's step (its own ring)
       const bool first = (fl >> 8) & 1, last = (fl >> 9) & 1;
@@ -916,14 +971,17 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #ifdef RB_PROF_SWEEP
         const long long t0 = clock64();
 #endif
+#ifndef RB_DBG_NOEPI
         mbar_wait(&sfree[slot], ((use_ph >> slot) & 1) ^ 1);
+#endif
 #ifdef RB_PROF_SWEEP
         prof_free += clock64() - t0;
 #endif
         use_ph ^= 1u << slot;
         tc_fence_after();
       }
-      const uint32_t d = tmem + (uint32_t)(slot * 2 * hp);
+      const uint32_t d = M64 ? tmem + ((uint32_t)(slot & 1) << 20) + (uint32_t)((slot >> 1) * 256)
+                             : tmem + (uint32_t)(slot * 2 * hp);
       for (int kc = 0; kc < a.dp_chunks; ++kc) {
         // descriptors = stage-0 descriptor + (byte offset >> 4): one add per operand (SMEM < 256 KB,
         // so the 14-bit address field never carries)
@@ -933,12 +991,19 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #ifdef RB_PROF_SWEEP
           const long long t1 = clock64();
 #endif
+#ifndef RB_DBG_MMAONLY
           if (!PAIR || (sg & 1) == 0) mbar_wait(&full[PAIR ? (sg & ~1) : sg], ps.ph);
+#endif
 #ifdef RB_PROF_SWEEP
           prof_full += clock64() - t1;
 #endif
           tc_fence_after();
-          if (n_mt == 2) {
+          if (M64) {  // tile (K-major) x B panel (MN-major, 4 boxes of 64 columns): M=64 N=256
+#pragma unroll
+            for (int kk = 0; kk < KCH / 16; ++kk)
+              umma_f16(d, bdesc0 + soff + kk * 2, adesc0 + soff + ((kk * 2048) >> 4), idesc,
+                       !(first && kc == 0 && kk == 0));
+          } else if (n_mt == 2) {
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -951,7 +1016,9 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
               umma_f16(d, adesc0 + soff + ((kk * 2048) >> 4), bdesc0 + soff + kk * 2, idesc,
                        !(first && kc == 0 && kk == 0));
           }
+#ifndef RB_DBG_MMAONLY
           umma_commit(&empty[sg]);
+#endif
           if (last && kc + 1 == a.dp_chunks) umma_commit(&sdone[slot]);
         }
         __syncwarp();
@@ -963,6 +1030,66 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       printf("sweep cta %d mma: total %lld wait_free %lld wait_full %lld steps %d\n", blockIdx.x, clock64() - prof_t0,
              prof_free, prof_full, s_end - s_begin);
 #endif
+  } else if (NOEPI_DBG) {
+  } else if (M64) {
+    // epilogue (M64): warp quadrant q = warp & 3 holds rows 16q..16q+15 of both lane halves; this
+    // warp drains 128 of the slot's 256 columns (half ch).  A lane of the slot's half owns one row.
+    const int q = warp & 3, ch = (warp - 1 - SW_MMA_WARPS) >> 2;
+    float* epi_buf = reinterpret_cast<float*>(smem + ST * (ASLOT + S_B_BYTES) + 1024) +
+                     (warp - 1 - SW_MMA_WARPS) * 16 * 36;
+    uint32_t done_ph = 0;
+    for (int j = w.done_ptr[blockIdx.x]; j < w.done_ptr[blockIdx.x + 1]; ++j) {
+      const int4 c = w.done[j];
+      const int g = c.x, n0 = c.y, slot = c.z;
+      const int p0 = a.row_partition[g];
+      const int h = a.row_partition[g + 1] - p0;
+      const int row = 16 * q + (lane & 15);
+      const bool mine = (lane >> 4) == (slot & 1) && row < h;
+      const int crow = mine ? a.row_perm[p0 + row] : 0;
+      if (lane == 0) mbar_wait_backoff(&sdone[slot], (done_ph >> slot) & 1, SW_EPI_SLEEP_NS);
+      __syncwarp();
+      done_ph ^= 1u << slot;
+      tc_fence_after();
+      uint32_t r[4][32];
+      const uint32_t t0 = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((slot >> 1) * 256 + ch * 128);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tmem_ld_32x32b_x32(t0 + k * 32, r[k]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[slot]);
+#ifdef RB_DBG_NOSTORE  // developer experiment: drain TMEM but do not store C
+      if (mine && r[0][0] == 0x7f7f7f7fu) a.C[crow] = 0.f;
+      continue;
+#endif
+      // A lane holds 32 consecutive columns of ITS row per chunk: stores straight from registers
+      // would be 16 rows x 16 B per instruction, and that L1 traffic measurably slows the tensor
+      // core's SMEM operand reads (config 5: 0.59 -> 0.83 kcycles per step).  Each chunk goes
+      // through a 16 x 32 float SMEM tile instead (row stride 36 floats: 2-way conflicts on the
+      // writes, none on the reads) and leaves as 16 coalesced 128-byte row stores.
+      const int nb = n0 + ch * 128;
+      const int slab_rows = min(16, h - 16 * q);
+      const int my_row = __shfl_sync(0xffffffffu, crow, (lane & 15) + 16 * (slot & 1));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if ((lane >> 4) == (slot & 1)) {
+          float* srow = epi_buf + (lane & 15) * 36;
+#pragma unroll
+          for (int t = 0; t < 32; t += 4)
+            *reinterpret_cast<float4*>(srow + t) =
+                make_float4(__uint_as_float(r[k][t]), __uint_as_float(r[k][t + 1]), __uint_as_float(r[k][t + 2]),
+                            __uint_as_float(r[k][t + 3]));
+        }
+        __syncwarp();
+        const int n = nb + k * 32 + lane;
+        for (int i = 0; i < slab_rows; ++i) {
+          const int cr = __shfl_sync(0xffffffffu, my_row, i);
+          if (n < a.N) a.C[(int64_t)cr * a.ldc + n] = epi_buf[i * 36 + lane];
+        }
+        __syncwarp();
+      }
+      (void)mine;
+    }
   } else {
     // epilogue: drain finished slots in commit order; TMEM lane = C column, a warp stores 32
     // consecutive floats (128 B) of one C row per instruction
@@ -980,7 +1107,8 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #ifdef RB_PROF_SWEEP
       const long long e0 = clock64();
 #endif
-      mbar_wait(&sdone[slot], (done_ph >> slot) & 1);
+      if (lane == 0) mbar_wait_backoff(&sdone[slot], (done_ph >> slot) & 1, SW_EPI_SLEEP_NS);
+      __syncwarp();
 #ifdef RB_PROF_SWEEP
       const long long e1 = clock64();
       prof_wait += e1 - e0;
@@ -2062,6 +2190,8 @@ static int ensure_kernel_attributes() {
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_tall2_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SP));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sweep64_smem()));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL, false>,
@@ -2280,7 +2410,14 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
         const char* e = std::getenv("RB_SWEEP_PAIR");
         return e && e[0] == '1';
       }();
-      if (pair_env)
+      static const bool m64_env = [] {
+        const char* e = std::getenv("RB_SWEEP_M64");
+        return !(e && e[0] == '0');
+      }();
+      if (p->sw_hp == 64 && m64_env)
+        spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false, true>
+            <<<(unsigned)p->sw_ctas, SW64_THREADS, sweep64_smem(), st>>>(tA, tmB, s, w);
+      else if (pair_env)
         spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, true>
             <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG), st>>>(tA, tmB, s, w);
       else if (p->sw_hp > 64 || big_env)

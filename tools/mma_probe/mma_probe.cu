@@ -14,6 +14,7 @@ using namespace rb;
 // 48 KB SMEM stages (the kernels' ring) instead of one fixed address.
 // 64 = warp 2 streams 40 KB of TMA bulk copies (global -> SMEM) per 8 MMAs into the stage being
 // consumed, as the producer does (SMEM write bandwidth shared with the tensor core's operand reads?).
+__device__ int g_random_fill = 0;
 template <int M, int N, int AMN, int BMN, int MODE = 0>
 __global__ void __launch_bounds__(128) probe(long long* out, int reps, const uint8_t* gsrc = nullptr) {
   extern __shared__ uint8_t raw[];
@@ -22,7 +23,13 @@ __global__ void __launch_bounds__(128) probe(long long* out, int reps, const uin
   __shared__ uint32_t tslot;
   __shared__ volatile int stop;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 196 * 1024 / 16; i += blockDim.x) reinterpret_cast<int4*>(sm)[i] = make_int4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < 196 * 1024 / 16; i += blockDim.x) {
+    uint32_t x = g_random_fill ? (uint32_t)(i * 2654435761u + blockIdx.x * 40503u) : 0u;
+    // random bf16 in [0.5, 1): sign 0, exponent 126, random mantissa (no NaN / Inf)
+    const uint32_t lo = 0x3F00u | ((x >> 3) & 0x7F), hi = 0x3F00u | ((x >> 13) & 0x7F);
+    const uint32_t w = g_random_fill ? (lo | (hi << 16)) : 0u;
+    reinterpret_cast<int4*>(sm)[i] = make_int4(w, w ^ 0x00010001u, w, w ^ 0x00030003u);
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_init(&bar2, 1);
@@ -65,7 +72,12 @@ __global__ void __launch_bounds__(128) probe(long long* out, int reps, const uin
           bd = (BMN ? sdesc_sw128(smem_u32(sm) + kk * 2048, 8192, 1024) : sdesc_sw128(smem_u32(sm) + kk * 32, 16, 1024)) +
                (st >> 4);
         }
-        const uint32_t d = (MODE & 8) ? tmem + (uint32_t)((r & 1) * N) : tmem;
+        uint32_t d = (MODE & 8) ? tmem + (uint32_t)((r & 1) * N) : tmem;
+        if (MODE & 2048) {  // 4 accumulators cycling every 8 MMAs (the sweep kernel's slots)
+          const int sl = (r >> 1) & 3;
+          d = M == 64 ? tmem + ((uint32_t)(sl & 1) << 20) + (uint32_t)((sl >> 1) * 256)
+                      : tmem + (uint32_t)(sl * 2 * N) + (uint32_t)((r & 1) * N);
+        }
         umma_f16(d, ad, bd, idesc, (r | kk) != 0);
       }
       if ((MODE & 1) && (r & per) == per) umma_commit(&spin);  // never waited on
@@ -227,7 +239,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) probe2(long lon
   __shared__ uint64_t bar, bar2, spin;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 196 * 1024 / 16; i += blockDim.x) reinterpret_cast<int4*>(sm)[i] = make_int4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < 196 * 1024 / 16; i += blockDim.x) {
+    uint32_t x = g_random_fill ? (uint32_t)(i * 2654435761u + blockIdx.x * 40503u) : 0u;
+    // random bf16 in [0.5, 1): sign 0, exponent 126, random mantissa (no NaN / Inf)
+    const uint32_t lo = 0x3F00u | ((x >> 3) & 0x7F), hi = 0x3F00u | ((x >> 13) & 0x7F);
+    const uint32_t w = g_random_fill ? (lo | (hi << 16)) : 0u;
+    reinterpret_cast<int4*>(sm)[i] = make_int4(w, w ^ 0x00010001u, w, w ^ 0x00030003u);
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_init(&bar2, 1);
@@ -289,6 +307,19 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   long long* d_out;
   cudaMalloc(&d_out, 64);
+  for (int rf = 0; rf < 2; ++rf) {
+  cudaMemcpyToSymbol(g_random_fill, &rf, sizeof(int));
+  printf("---- SMEM operands: %s\n", rf ? "random bf16 in [0.5, 1)" : "zeros");
+  run<128, 64, 1, 0>("swap-AB (short kernel today)", d_out, sms);
+  run<64, 256, 0, 1>("rows-as-M M=64 (tile K, B mn)", d_out, sms);
+  run<128, 256, 0, 1>("tall-like 1-CTA (A K, B mn)", d_out, sms);
+  run<128, 64, 1, 0, 63 + 128 + 256>("swap everything, no fence, desc add", d_out, sms);
+  run<64, 256, 0, 1, 63 + 128 + 256>("M=64 everything, no fence, desc add", d_out, sms);
+  run<64, 256, 0, 1, 63 + 128 + 256 + 2048>("M=64 everything + 4 slots", d_out, sms);
+  run<128, 64, 1, 0, 63 + 128 + 256 + 2048>("swap everything + 4 slots", d_out, sms);
+  run<64, 256, 0, 1, 2048>("M=64 only 4 slots", d_out, sms);
+  run<128, 64, 1, 0, 2048>("swap only 4 slots", d_out, sms);
+  }
   run<128, 64, 1, 0>("swap-AB (short kernel today)", d_out, sms);
   run<128, 64, 0, 0>("swap-AB, both K-major", d_out, sms);
   run<128, 128, 1, 0>("swap-AB N=128", d_out, sms);
