@@ -808,7 +808,7 @@ constexpr int SW_STAGES_BIG = 4, SW_STAGES_SMALL = 5;
 constexpr uint32_t SW_ASLOT_BIG = 128 * KCH * 2, SW_ASLOT_SMALL = 64 * KCH * 2;
 constexpr uint32_t sweep_smem(int st, uint32_t aslot) { return st * (aslot + S_B_BYTES) + 1024 + 512; }
 constexpr uint32_t SW64_EPI_BYTES = 8 * 16 * 36 * 4;  // M64 epilogue staging: 16 x 36 floats per warp
-constexpr uint32_t sweep64_smem() { return SW_STAGES_BIG * (SW_ASLOT_BIG + S_B_BYTES) + 1024 + 1024 + SW64_EPI_BYTES; }
+constexpr uint32_t sweep64_smem(int st, uint32_t aslot) { return st * (aslot + S_B_BYTES) + 1024 + 1024 + SW64_EPI_BYTES; }
 
 struct SweepArgs {
   const int4* steps;        // (A tile row, first B row, n0, slot | first << 8 | last << 9)
@@ -862,6 +862,11 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     spmm_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SpmmArgs a,
                       SweepArgs w) {
   extern __shared__ uint8_t smem_raw[];
+#ifdef RB_PROF_SWEEP
+  long long k_t0 = clock64();
+  unsigned long long k_g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_g0));
+#endif
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (ASLOT + S_B_BYTES));
   uint64_t* empty = full + ST;
@@ -1026,7 +1031,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
       }
     }
 #ifdef RB_PROF_SWEEP
-    if (blockIdx.x % 37 == 0 && lane == 0)
+    if (blockIdx.x % 8 == 0 && lane == 0)
       printf("sweep cta %d mma: total %lld wait_free %lld wait_full %lld steps %d\n", blockIdx.x, clock64() - prof_t0,
              prof_free, prof_full, s_end - s_begin);
 #endif
@@ -1036,7 +1041,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     // warp drains 128 of the slot's 256 columns (half ch).  A lane of the slot's half owns one row.
     const int q = warp & 3, ch = (warp - 1 - SW_MMA_WARPS) >> 2;
     float* epi_buf = reinterpret_cast<float*>(smem + ST * (ASLOT + S_B_BYTES) + 1024) +
-                     (warp - 1 - SW_MMA_WARPS) * 16 * 36;
+                     (warp - 1 - SW_MMA_WARPS) * 16 * 36;  // 16 x 33 used
     uint32_t done_ph = 0;
     for (int j = w.done_ptr[blockIdx.x]; j < w.done_ptr[blockIdx.x + 1]; ++j) {
       const int4 c = w.done[j];
@@ -1065,26 +1070,23 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
       // A lane holds 32 consecutive columns of ITS row per chunk: stores straight from registers
       // would be 16 rows x 16 B per instruction, and that L1 traffic measurably slows the tensor
       // core's SMEM operand reads (config 5: 0.59 -> 0.83 kcycles per step).  Each chunk goes
-      // through a 16 x 32 float SMEM tile instead (row stride 36 floats: 2-way conflicts on the
-      // writes, none on the reads) and leaves as 16 coalesced 128-byte row stores.
+      // through a 16 x 32 float SMEM tile instead (row stride 33 floats: conflict-free scalar writes
+      // and reads) and leaves as 16 coalesced 128-byte row stores.
       const int nb = n0 + ch * 128;
       const int slab_rows = min(16, h - 16 * q);
       const int my_row = __shfl_sync(0xffffffffu, crow, (lane & 15) + 16 * (slot & 1));
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if ((lane >> 4) == (slot & 1)) {
-          float* srow = epi_buf + (lane & 15) * 36;
+        if ((lane >> 4) == (slot & 1)) {  // row stride 33: lane i writes bank (i + t) % 32, no conflicts
+          float* srow = epi_buf + (lane & 15) * 33;
 #pragma unroll
-          for (int t = 0; t < 32; t += 4)
-            *reinterpret_cast<float4*>(srow + t) =
-                make_float4(__uint_as_float(r[k][t]), __uint_as_float(r[k][t + 1]), __uint_as_float(r[k][t + 2]),
-                            __uint_as_float(r[k][t + 3]));
+          for (int t = 0; t < 32; ++t) srow[t] = __uint_as_float(r[k][t]);
         }
         __syncwarp();
         const int n = nb + k * 32 + lane;
         for (int i = 0; i < slab_rows; ++i) {
           const int cr = __shfl_sync(0xffffffffu, my_row, i);
-          if (n < a.N) a.C[(int64_t)cr * a.ldc + n] = epi_buf[i * 36 + lane];
+          if (n < a.N) a.C[(int64_t)cr * a.ldc + n] = epi_buf[i * 33 + lane];
         }
         __syncwarp();
       }
@@ -1190,6 +1192,13 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
+#ifdef RB_PROF_SWEEP
+  if (threadIdx.x == 0 && blockIdx.x % 8 == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    printf("sweep cta %d kernel: cycles %lld ns %llu start_ns %llu\n", blockIdx.x, clock64() - k_t0, g1 - k_g0, k_g0);
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2191,7 +2200,11 @@ static int ensure_kernel_attributes() {
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sweep64_smem()));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sweep64_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
+  RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL, false, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sweep64_smem(SW_STAGES_SMALL, SW_ASLOT_SMALL)));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG)));
   RB_CUDA_TRY(cudaFuncSetAttribute(spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL, false>,
@@ -2414,9 +2427,12 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
         const char* e = std::getenv("RB_SWEEP_M64");
         return !(e && e[0] == '0');
       }();
-      if (p->sw_hp == 64 && m64_env)
+      if (p->sw_hp == 64 && m64_env && !big_env)  // RB_SWEEP_BIG=0: the 5 x 40 KB ring
+        spmm_sweep_kernel<SW_STAGES_SMALL, SW_ASLOT_SMALL, false, true>
+            <<<(unsigned)p->sw_ctas, SW64_THREADS, sweep64_smem(SW_STAGES_SMALL, SW_ASLOT_SMALL), st>>>(tA, tmB, s, w);
+      else if (p->sw_hp == 64 && m64_env)
         spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, false, true>
-            <<<(unsigned)p->sw_ctas, SW64_THREADS, sweep64_smem(), st>>>(tA, tmB, s, w);
+            <<<(unsigned)p->sw_ctas, SW64_THREADS, sweep64_smem(SW_STAGES_BIG, SW_ASLOT_BIG), st>>>(tA, tmB, s, w);
       else if (pair_env)
         spmm_sweep_kernel<SW_STAGES_BIG, SW_ASLOT_BIG, true>
             <<<(unsigned)p->sw_ctas, SW_THREADS, sweep_smem(SW_STAGES_BIG, SW_ASLOT_BIG), st>>>(tA, tmB, s, w);
