@@ -83,6 +83,43 @@ def streams_sweep(rows, slab, ctas, slots, N=1024, nbc=4096):
     return per
 
 
+def streams_snake(rows, slab, ctas, slots, N=1024, nbc=4096):
+    """As streams_sweep, but the CTA's sweep reverses direction at the ends of the block-column
+    range (boustrophedon): a row entering a slot collects its blocks ahead of the current column in
+    the current direction, then the rest on the way back."""
+    per = [[] for _ in range(ctas)]
+    for s in range(N // slab):
+        a = lpt([len(r) for r in rows], ctas)
+        for c in range(ctas):
+            queue = list(a[c])
+            active = []  # [g, remaining set]
+            phase, direction = 0, 1
+            out = per[c]
+            while queue or active:
+                while len(active) < slots and queue:
+                    g = queue.pop(0)
+                    active.append([g, set(range(len(rows[g])))])
+                best, bd = None, None
+                for k, (g, rem) in enumerate(active):
+                    r = rows[g]
+                    for t in rem:
+                        d = (r[t] - phase) * direction
+                        if d >= 0 and (bd is None or d < bd):
+                            best, bd = (k, t), d
+                if best is None:  # nothing ahead: reverse
+                    direction = -direction
+                    continue
+                k, t = best
+                g, rem = active[k]
+                b = int(rows[g][t])
+                out.append((g, t, b, s))
+                phase = b
+                rem.discard(t)
+                if not rem:
+                    active.pop(k)
+    return per
+
+
 def replay(per, slab, l2mb, jitter=0.15, seed=0, a_bytes=8192, panel_rows=64, a_bypass=False):
     rng = np.random.default_rng(seed)
     b_bytes = panel_rows * slab * 2
@@ -129,6 +166,8 @@ def main():
     rows = structure(nbr=args.nbr)
     if args.design == "current":
         per = streams_current(rows, args.slab, args.ctas)
+    elif args.design == "snake":
+        per = streams_snake(rows, args.slab, args.ctas, args.slots)
     else:
         per = streams_sweep(rows, args.slab, args.ctas, args.slots)
     miss, tot = replay(per, args.slab, args.l2mb, args.jitter, a_bypass=args.a_bypass)
