@@ -584,7 +584,12 @@ __device__ __forceinline__ void csr_item(const SkinnyArgs& a, const CsrArgs& c, 
 }
 
 template <typename T, int LPR, bool ALIGNED>
-__global__ void __launch_bounds__(256, 2) spmm_csr_kernel(SkinnyArgs a, CsrArgs c, int cols,
+// 4 resident CTAs per SM (<= 64 registers, a few spills): twice the gathers in flight of the
+// 2-CTA build; config 3 1.08 -> 0.86 ms, 2b 7.50 -> 6.50 ms, config 1 +6 % (latency-bound, tiny).
+#ifndef RB_CSR_MIN_BLOCKS
+#define RB_CSR_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, RB_CSR_MIN_BLOCKS) spmm_csr_kernel(SkinnyArgs a, CsrArgs c, int cols,
                                                           unsigned long long* sched) {
   constexpr int GPW = 32 / LPR;
   const int lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
