@@ -91,6 +91,11 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
 
 
+def _compact_h() -> int:
+    from paper_2202_05868_b200 import config as rbconfig
+    return rbconfig.compact_h()
+
+
 def profile_traffic(config: str):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
@@ -352,8 +357,9 @@ def run_ours(args, world, rank):
         esz = 4 if prec == "fp32" else 2
         alg_bytes = dv.csr.nnz * (esz + 4) + dA.n_cols * N * esz + dv.n_rows * N * 4
         achieved_gbs = alg_bytes / (ms_local * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "spmm_skinny_staged_kernel (h<=4 classes)" if prec != "fp32"
-                else "spmm_skinny*_kernel<float> + spmm_simt_f32_kernel",
+        roof = {"bound": "hbm", "kernel": ("spmm_simt_f32_kernel + skinny tiles" if prec == "fp32" else
+                                            "spmm_csr_kernel over compact payloads" if _compact_h() else
+                                            "spmm_skinny_staged_kernel (h<=4 classes)"),
                 "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved_gbs / peaks["hbm_gbs"], 5), "traffic": profile_traffic(args.config),
                 "peak_source": peaks["source"] + " (HBM copy bandwidth)",
