@@ -367,6 +367,10 @@ def run_ours(args, world, rank):
                 "algorithmic_bytes_per_step": alg_bytes,
                 "executed_tflops": round(exec_tflops, 3),
                 "useful_tflops": round(achieved_tflops, 4)}
+    if roof["traffic"] and world == 1 and args.scale == 1:
+        # the ncu DRAM bytes of one step over this run's step time: how close the step is to HBM
+        roof["traffic_gbs"] = round(roof["traffic"] / (ms_local * 1e-3) / 1e9, 1)
+        roof["traffic_frac_of_hbm"] = round(roof["traffic_gbs"] / peaks["hbm_gbs"], 4)
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
