@@ -40,6 +40,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=30)
+    p.add_argument("--fused-gather", action="store_true",
+                   help="N > 1: also time the fused all-gather (SpMM epilogues store into every rank's "
+                        "symmetric-memory C over NVLink, dist.FusedGather) as 'gather_fused'")
     return p.parse_args()
 
 
@@ -331,6 +334,8 @@ def run_ours(args, world, rank):
     value = useful / (ms * 1e-3) / 1e9
 
     gather = run_gather(args, dv, B, C, prec, shard, world, flush, useful) if world > 1 else None
+    gather_fused = run_gather_fused(args, dv, B, prec, shard, world, flush, useful) if (
+        world > 1 and args.fused_gather) else None
 
     # ---- end to end through the reference-facing path: pinned float64 B -> device -> kernel -> float64 C
     e2e = run_e2e(args, dv, dA, B, prec, rank, world)
@@ -376,7 +381,7 @@ def run_ours(args, world, rank):
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
         "config": workload_config(cfg, dA.n_rows, dA.n_cols, dA.nnz, world),
-        "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "gather": gather,
+        "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "gather": gather, "gather_fused": gather_fused,
         "csr_comparator": csr,
         "clocks": sampler.summary(),
         "stages": dict(stages, rho_prime=round(dA.nnz / max(dv.stored_area(), 1), 5),
@@ -418,6 +423,40 @@ def run_gather(args, dv, B, C, prec, shard, world, flush, useful):
     return {"ms_per_step": round(ms, 4), "value": round(useful / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
             "what": "SpMM of the rank's shard + NCCL all-gather of C (fp32) + un-permute to source rows, "
                     "max over ranks; every rank ends with the full C"}
+
+
+def run_gather_fused(args, dv, B, prec, shard, world, flush, useful):
+    """N > 1, --fused-gather: the same product and collective result as run_gather, but the SpMM
+    epilogues store each rank's rows at their source rows into every rank's symmetric-memory C over
+    NVLink (rb_spmm_execute_fanout), then one device-side barrier: no NCCL call, no un-permute pass.
+    Checked once against the NCCL path (bit-identical rows) before timing."""
+    from paper_2202_05868_b200 import dist as rbdist
+
+    try:
+        fg = rbdist.FusedGather(int(shard["row_perm"].numel()), B.shape[1], B.device)
+        C = torch.empty((dv.n_rows, B.shape[1]), dtype=torch.float32, device=B.device)
+        dv.spmm(B, out=C, precision=prec)
+        ref = rbdist.gather_c(C, shard["row_perm"], shard["ranges"])
+        for _ in range(2):
+            got = fg.run(dv, B, precision=prec)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(got, ref))
+        barrier(world)
+        steps = max(3, min(args.steps, 10))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for s, e in ev:
+            flush.zero_()
+            s.record()
+            fg.run(dv, B, precision=prec)
+            e.record()
+        torch.cuda.synchronize()
+        ms = allreduce_max(sum(s.elapsed_time(e) for s, e in ev) / steps, world)
+        return {"ms_per_step": round(ms, 4), "value": round(useful / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                "matches_nccl_gather": same,
+                "what": "SpMM of the rank's shard with fan-out epilogue stores into every rank's full C "
+                        "(symmetric memory over NVLink) + device barrier, max over ranks"}
+    except Exception as exc:  # noqa: BLE001 — report, do not lose the rest of the line
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
 
 def run_csr_comparator(args, dA, B, prec, flush):

@@ -187,6 +187,19 @@ int rb_spmm_execute(const rb_spmm_plan* plan, const void* B, int64_t ldb, float*
  * and the same NaN / Inf propagation. */
 int rb_spmm_execute_f64(const rb_spmm_plan* plan, const double* B, int64_t ldb, double* C, int64_t ldc,
                         void* stream);
+/* Fused all-gather of C (north_star's optional collective): as rb_spmm_execute, and
+ * every C element the kernels store is also stored, at the same offset, into peers[0..n_peers) —
+ * the other ranks' full-size float32 C buffers mapped into this process over NVLink (P2P /
+ * symmetric memory; any device pointers of C's layout work, e.g. several buffers on one GPU).  The
+ * copies are written by the SpMM epilogues themselves, so the gather overlaps the math tile by tile
+ * and needs no separate collective or un-permute pass.  c_rows (device int32 [plan n_rows], NULL =
+ * the plan's row_perm) maps the plan's permuted row p to the output row c_rows[p]: a rank's
+ * sub-matrix plan (dist.shard_vbr) passes the global source rows of its shard, so every buffer
+ * receives the rank's rows exactly where multiply.py:90 puts them.  C, peers and ldc as in
+ * rb_spmm_execute; with n_peers > 0 every pointer must be 16-byte aligned.  n_peers <= 7; not for
+ * RB_F64 plans.  The caller orders the peers' reads after the writes (a barrier across ranks). */
+int rb_spmm_execute_fanout(const rb_spmm_plan* plan, const void* B, int64_t ldb, float* C, int64_t ldc,
+                           float* const* peers, int32_t n_peers, const int32_t* c_rows, void* stream);
 int rb_spmm_plan_destroy(rb_spmm_plan* plan);
 /* 2:4 sparse tensor-core form of the tall block rows (sparse24.cu): stage = 128 logical K of a
  * block row's padded block sequence; 64 compressed values + 4 TMEM metadata words per tile row and

@@ -80,6 +80,7 @@ def lib():
         L.rb_spmm_plan_info.argtypes = [P, ctypes.POINTER(SpmmInfo)]
         L.rb_spmm_execute.argtypes = [P, P, I64, P, I64, P]
         L.rb_spmm_execute_f64.argtypes = [P, P, I64, P, I64, P]
+        L.rb_spmm_execute_fanout.argtypes = [P, P, I64, P, I64, P, I32, P, P]
         L.rb_spmm_plan_destroy.argtypes = [P]
         L.rb_convert_f64.argtypes = [P, I64, I64, I64, P, I32, I64, P]
         L.rb_convert_f64_checked.argtypes = [P, I64, I64, I64, P, I32, I64, P, P]
@@ -102,7 +103,7 @@ def lib():
         for name in ("rb_csr_plan_create", "rb_csr_execute", "rb_csr_plan_destroy"):
             getattr(L, name).restype = INT
         for name in ("rb_block_1sa_workspace_size", "rb_block_1sa", "rb_vbr_workspace_size", "rb_vbr_plan",
-                     "rb_vbr_emit", "rb_vbr_compact_count", "rb_vbr_compact_emit", "rb_spmm_plan_create", "rb_spmm_plan_create_ex", "rb_spmm_plan_info", "rb_spmm_execute", "rb_spmm_execute_f64",
+                     "rb_vbr_emit", "rb_vbr_compact_count", "rb_vbr_compact_emit", "rb_spmm_plan_create", "rb_spmm_plan_create_ex", "rb_spmm_plan_info", "rb_spmm_execute", "rb_spmm_execute_f64", "rb_spmm_execute_fanout",
                      "rb_spmm_plan_destroy", "rb_convert_f64", "rb_convert_f64_checked", "rb_widen_f32", "rb_group_stats_workspace_size",
                      "rb_group_stats"):
             getattr(L, name).restype = INT

@@ -43,6 +43,17 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+// Fused all-gather of C (rb_spmm_execute_fanout): every C store of the SpMM kernels is repeated
+// into up to RB_MAX_FAN further buffers of C's layout at the same element offset.  The buffers are
+// the other ranks' full-size C, mapped into this process (NVLink P2P / symmetric memory), so a rank
+// writes its rows, already in source row order, straight into every peer's C: the all-gather and
+// the un-permute of multiply.py:90 ride on the epilogue's own stores.  n = 0: plain stores.
+constexpr int RB_MAX_FAN = 7;
+struct CFan {
+  float* p[RB_MAX_FAN];
+  int32_t n;
+};
+
 // Thread-local error string for rb_last_error_string().
 void set_error(const std::string& s);
 int fail(int code, const std::string& s);

@@ -84,6 +84,7 @@ struct SpmmArgs {
   int32_t* cnt;            // split-K arrival counters: [slot][8 warps] (zero between launches)
   const uint32_t* sp_meta;     // 2:4 path: TMEM metadata words (sparse24.cu layout)
   const int64_t* sp_tile_row;  // 2:4 path: first compressed row of each tall block row
+  CFan fan;                    // further copies of every C store (fused all-gather); fan.n = 0: none
 };
 
 // Tall work unit = two int4: (g, m, n0, k0) and (k1, split, n_splits, slot).  Units with
@@ -121,6 +122,19 @@ __device__ __forceinline__ void store_row_chunk(float* dst, const uint32_t (&r)[
     for (int j = 0; j < 32; ++j)
       if (j < ncols) dst[j] = __uint_as_float(r[j]);
   }
+}
+
+// store_row_chunk into C and every fan-out copy (same element offset in each buffer)
+__device__ __forceinline__ void store_row_chunk_fan(const CFan& fan, const float* C, float* dst,
+                                                    const uint32_t (&r)[32], int ncols, bool vec) {
+  store_row_chunk(dst, r, ncols, vec);
+  const int64_t off = dst - C;
+  for (int f = 0; f < fan.n; ++f) store_row_chunk(fan.p[f] + off, r, ncols, vec);
+}
+
+__device__ __forceinline__ void st_fan(const CFan& fan, float* C, int64_t off, float v) {
+  C[off] = v;
+  for (int f = 0; f < fan.n; ++f) fan.p[f][off] = v;
 }
 
 struct PipeState {
@@ -317,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
               r[4 * j + 2] = __float_as_uint(t.z);
               r[4 * j + 3] = __float_as_uint(t.w);
             }
-            if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+            if (valid) store_row_chunk_fan(a.fan, a.C, dst + c, r, ncol - c, vec);
           }
           if (lane == 0) *ctr = 0;  // ready for the next launch (stream ordered)
         }
@@ -332,7 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = 0u;
         }
-        if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+        if (valid) store_row_chunk_fan(a.fan, a.C, dst + c, r, ncol - c, vec);
       }
       if (nk > 0) {
         tc_fence_before();
@@ -569,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
               r[4 * j + 2] = __float_as_uint(t.z);
               r[4 * j + 3] = __float_as_uint(t.w);
             }
-            if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+            if (valid) store_row_chunk_fan(a.fan, a.C, dst + c, r, ncol - c, vec);
           }
           if (lane == 0) *ctr = 0;
         }
@@ -579,7 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
         tmem_ld_wait();
-        if (valid) store_row_chunk(dst + c, r, ncol - c, vec);
+        if (valid) store_row_chunk_fan(a.fan, a.C, dst + c, r, ncol - c, vec);
       }
       tc_fence_before();
       __syncwarp();
@@ -732,11 +746,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               if (j0 + j < h) {
-                float* dst = a.C + (int64_t)a.row_perm[p0 + j0 + j] * a.ldc + n;
+                const int64_t off = (int64_t)a.row_perm[p0 + j0 + j] * a.ldc + n;
                 if (a.c_evict_first)
-                  st_global_hint(dst, __uint_as_float(r[j]), pol_c);
+                  st_global_hint(a.C + off, __uint_as_float(r[j]), pol_c);
                 else
-                  *dst = __uint_as_float(r[j]);
+                  a.C[off] = __uint_as_float(r[j]);
+                for (int f = 0; f < a.fan.n; ++f) a.fan.p[f][off] = __uint_as_float(r[j]);
               }
             }
           }
@@ -816,6 +831,8 @@ struct SweepArgs {
   const int4* done;         // row completions in commit order: (g, n0, slot, -)
   const int32_t* done_ptr;
   int32_t hp;
+  float b_frac;      // share of B lines loaded with L2 evict_last (1: all; RB_SWEEP_BFRAC)
+  int32_t c_stream;  // 1: C stores with L2 evict_first (RB_SWEEP_CST)
 };
 
 // PAIR: the full barrier of an even stage covers it and the next one (2 arrivals per phase), so the
@@ -909,7 +926,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmA);
     const uint64_t pol_a = policy_evict_first();
-    const uint64_t pol_b = policy_evict_last();
+    const uint64_t pol_b = w.b_frac >= 1.f ? policy_evict_last() : policy_evict_last_frac(w.b_frac);
     PipeState rings[SW_MMA_WARPS];
     StepReader rd;
     rd.init(w.steps, s_begin, s_end, lane);
@@ -1040,6 +1057,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     // epilogue (M64): warp quadrant q = warp & 3 holds rows 16q..16q+15 of both lane halves; this
     // warp drains 128 of the slot's 256 columns (half ch).  A lane of the slot's half owns one row.
     const int q = warp & 3, ch = (warp - 1 - SW_MMA_WARPS) >> 2;
+    const uint64_t pol_c = policy_evict_first();
     float* epi_buf = reinterpret_cast<float*>(smem + ST * (ASLOT + S_B_BYTES) + 1024) +
                      (warp - 1 - SW_MMA_WARPS) * 16 * 36;  // 16 x 33 used
     uint32_t done_ph = 0;
@@ -1086,7 +1104,14 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
         const int n = nb + k * 32 + lane;
         for (int i = 0; i < slab_rows; ++i) {
           const int cr = __shfl_sync(0xffffffffu, my_row, i);
-          if (n < a.N) a.C[(int64_t)cr * a.ldc + n] = epi_buf[i * 33 + lane];
+          if (n < a.N) {
+            const int64_t off = (int64_t)cr * a.ldc + n;
+            if (w.c_stream)
+              st_global_hint(a.C + off, epi_buf[i * 33 + lane], pol_c);
+            else
+              a.C[off] = epi_buf[i * 33 + lane];
+            for (int f = 0; f < a.fan.n; ++f) a.fan.p[f][off] = epi_buf[i * 33 + lane];
+          }
         }
         __syncwarp();
       }
@@ -1152,7 +1177,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
 #pragma unroll
           for (int jj = 0; jj < 64; ++jj) {
             const int row = __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31);
-            if (nvalid && jj < h) a.C[(int64_t)row * a.ldc + n] = __uint_as_float(r[mt][jj]);
+            if (nvalid && jj < h) st_fan(a.fan, a.C, (int64_t)row * a.ldc + n, __uint_as_float(r[mt][jj]));
           }
         }
       } else {
@@ -1169,7 +1194,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
             for (int jj = 0; jj < 64; ++jj) {
               const int row = j0 == 0 ? __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31)
                                       : a.row_perm[p0 + j0 + jj];
-              if (nvalid && j0 + jj < h) a.C[(int64_t)row * a.ldc + n] = __uint_as_float(r[jj]);
+              if (nvalid && j0 + jj < h) st_fan(a.fan, a.C, (int64_t)row * a.ldc + n, __uint_as_float(r[jj]));
             }
           }
         }
@@ -1243,7 +1268,12 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_kernel(SpmmArgs a, const 
     }
   }
   if (nv) {
-    for (int r = 0; r < rows; ++r) C[(int64_t)a.row_perm[p0 + r0 + r] * a.ldc + n] = acc[r];
+    for (int r = 0; r < rows; ++r) {
+      const int64_t off = (int64_t)a.row_perm[p0 + r0 + r] * a.ldc + n;
+      C[off] = acc[r];
+      if constexpr (sizeof(T) == sizeof(float))  // fan-out is float32 C only (the host refuses fp64)
+        for (int f = 0; f < a.fan.n; ++f) a.fan.p[f][off] = acc[r];
+    }
   }
 }
 
@@ -1252,18 +1282,21 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_kernel(SpmmArgs a, const 
 // stores (multiply.py:85-86 leaves them exactly 0).
 __global__ void __launch_bounds__(256) zero_rows_kernel(const int32_t* __restrict__ pos, int64_t n,
                                                         const int32_t* __restrict__ row_perm, float* C, int64_t ldc,
-                                                        int32_t N) {
+                                                        int32_t N, CFan fan) {
   const int lane = threadIdx.x & 31;
   const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    float* dst = C + (int64_t)row_perm[pos[w]] * ldc;
-    if (vec) {
-      const int n4 = N >> 2;
-      for (int c = lane; c < n4; c += 32) reinterpret_cast<float4*>(dst)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c = (n4 << 2) + lane; c < N; c += 32) dst[c] = 0.f;
-    } else {
-      for (int c = lane; c < N; c += 32) dst[c] = 0.f;
+    const int64_t off = (int64_t)row_perm[pos[w]] * ldc;
+    for (int f = -1; f < fan.n; ++f) {  // C, then every fan-out copy
+      float* dst = (f < 0 ? C : fan.p[f]) + off;
+      if (vec) {
+        const int n4 = N >> 2;
+        for (int c = lane; c < n4; c += 32) reinterpret_cast<float4*>(dst)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = (n4 << 2) + lane; c < N; c += 32) dst[c] = 0.f;
+      } else {
+        for (int c = lane; c < N; c += 32) dst[c] = 0.f;
+      }
     }
   }
 }
@@ -2215,10 +2248,10 @@ static int ensure_kernel_attributes() {
 }
 
 static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
-                               cudaStream_t stream);
+                               cudaStream_t stream, const CFan& fan, const int32_t* c_rows);
 
 static int spmm_execute_entry(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
-                              void* stream_);
+                              void* stream_, const CFan* fan = nullptr, const int32_t* c_rows = nullptr);
 
 extern "C" int rb_spmm_execute(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
                                void* stream_) {
@@ -2234,14 +2267,33 @@ extern "C" int rb_spmm_execute_f64(const rb_spmm_plan* p, const double* B, int64
   return spmm_execute_entry(p, B, ldb, reinterpret_cast<float*>(C), ldc, stream_);
 }
 
+extern "C" int rb_spmm_execute_fanout(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
+                                      float* const* peers, int32_t n_peers, const int32_t* c_rows, void* stream_) {
+  rb::NvtxRange nvtx_range_("rb_spmm_execute_fanout");
+  if (!p) return fail(RB_EINVAL, "null plan");
+  if (p->b_dtype == RB_F64) return fail(RB_EINVAL, "fan-out needs a float32-C plan (not RB_F64)");
+  if (n_peers < 0 || n_peers > RB_MAX_FAN) return fail(RB_EINVAL, "n_peers must be in [0, 7]");
+  if (n_peers > 0 && !peers) return fail(RB_EINVAL, "null peers");
+  CFan fan{};
+  fan.n = n_peers;
+  for (int i = 0; i < n_peers; ++i) {
+    if (!peers[i] && p->v.n_rows > 0) return fail(RB_EINVAL, "null peer buffer");
+    if ((reinterpret_cast<uintptr_t>(peers[i]) & 15) || (reinterpret_cast<uintptr_t>(C) & 15) || (ldc & 3))
+      return fail(RB_EINVAL, "fan-out buffers must be 16-byte aligned (ldc a multiple of 4)");
+    fan.p[i] = peers[i];
+  }
+  return spmm_execute_entry(p, B, ldb, C, ldc, stream_, &fan, c_rows);
+}
+
 static int spmm_execute_entry(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
-                              void* stream_) {
+                              void* stream_, const CFan* fan, const int32_t* c_rows) {
   if (!p) return fail(RB_EINVAL, "null plan");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   std::lock_guard<std::mutex> lk(p->mu);
   if (!p->done) RB_CUDA_TRY(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
   if (p->done_valid && p->done_stream != stream) RB_CUDA_TRY(cudaStreamWaitEvent(stream, p->done, 0));
-  const int rc = spmm_execute_locked(p, B, ldb, C, ldc, stream);
+  static const CFan no_fan{};
+  const int rc = spmm_execute_locked(p, B, ldb, C, ldc, stream, fan ? *fan : no_fan, c_rows);
   if (rc) return rc;
   RB_CUDA_TRY(cudaEventRecord(p->done, stream));
   p->done_stream = stream;
@@ -2250,12 +2302,14 @@ static int spmm_execute_entry(const rb_spmm_plan* p, const void* B, int64_t ldb,
 }
 
 static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb, float* C, int64_t ldc,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, const CFan& fan, const int32_t* c_rows) {
+  // output row of permuted row p: the plan's row_perm, or the caller's map (fan-out shards)
+  const int32_t* out_rows = c_rows ? c_rows : p->v.row_perm;
   if (ldc < p->N || ldb < p->N) return fail(RB_EINVAL, "leading dimension smaller than N");
   if (!C && p->v.n_rows > 0) return fail(RB_EINVAL, "null C");
   SpmmArgs a;
   a.row_partition = p->v.row_partition;
-  a.row_perm = p->v.row_perm;
+  a.row_perm = out_rows;
   a.blk_ptr = p->v.blk_ptr;
   a.blk_col = p->v.blk_col;
   a.grp_tile_row = p->v.grp_tile_row;
@@ -2274,6 +2328,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
   a.cnt = p->d_cnt;
   a.sp_meta = nullptr;
   a.sp_tile_row = nullptr;
+  a.fan = fan;
   // Independent launches (disjoint C rows): zero rows, each skinny height class, the fp32 SIMT
   // kernel, the tall and the short tensor-core kernels.  With more than one, they are forked over
   // the caller's stream and up to three auxiliary streams and joined back (small latency-bound
@@ -2284,13 +2339,13 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
       // fp64 C: a row of N doubles is 2N zero floats
       const int w = p->b_dtype == RB_F64 ? 2 : 1;
-      zero_rows_kernel<<<grid, 256, 0, st>>>(p->d_zero, p->n_zero, p->v.row_perm, C, ldc * w, (int32_t)p->N * w);
+      zero_rows_kernel<<<grid, 256, 0, st>>>(p->d_zero, p->n_zero, out_rows, C, ldc * w, (int32_t)p->N * w, fan);
       RB_CUDA_TRY(cudaGetLastError());
       return RB_OK;
     });
   SkinnyArgs k{};
   k.row_partition = p->v.row_partition;
-  k.row_perm = p->v.row_perm;
+  k.row_perm = out_rows;
   k.blk_ptr = p->v.blk_ptr;
   k.blk_col = p->v.blk_col;
   k.grp_tile_row = p->v.grp_tile_row;
@@ -2304,6 +2359,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
   k.N = (int32_t)p->N;
   k.ws = p->d_skinny_ws;
   k.cnt = p->d_skinny_cnt;
+  k.fan = fan;
   for (int c = 0; c < SKINNY_CLASSES; ++c) {
     if (p->skinny_off[c + 1] == p->skinny_off[c]) continue;
     tasks.push_back([&, c](cudaStream_t st) {
@@ -2368,7 +2424,8 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
         }
         if (p->n_res_items > 0) {  // C += residuals x B (groups of 4 with more than two nonzeros), same stream
           SkinnyArgs kr{};
-          kr.row_perm = p->v.row_perm;
+          kr.row_perm = out_rows;
+          kr.fan = fan;
           kr.items = p->d_res_items;
           kr.n_items = p->n_res_items;
           kr.B = B;
@@ -2411,7 +2468,28 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
   if (tc && p->n_sw_steps > 0)
     tasks.push_back([&](cudaStream_t st) {
       SpmmArgs s = a;
-      SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp};
+      // L2 experiments (developer knobs): RB_SWEEP_BFRAC = % of B lines loaded evict_last (default
+      // 100), RB_SWEEP_CST=1 = C stores evict_first, RB_SWEEP_L2SET = MB of persisting-L2 set-aside
+      // (cudaLimitPersistingL2CacheSize, process-wide; evict_last lines live there)
+      static const float b_frac = [] {
+        const char* e = std::getenv("RB_SWEEP_BFRAC");
+        const int v = e ? std::atoi(e) : 100;
+        return v <= 0 || v >= 100 ? 1.f : (float)v / 100.f;
+      }();
+      static const int c_stream = [] {
+        const char* e = std::getenv("RB_SWEEP_CST");
+        return e && e[0] == '1' ? 1 : 0;
+      }();
+      static const int l2set = [] {
+        const char* e = std::getenv("RB_SWEEP_L2SET");
+        return e ? std::atoi(e) : -1;
+      }();
+      if (l2set >= 0) {
+        size_t cur = 0;
+        RB_CUDA_TRY(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+        if (cur != ((size_t)l2set << 20)) RB_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)l2set << 20));
+      }
+      SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp, b_frac, c_stream};
       const CUtensorMap& tA = p->sw_hp == 16 ? p->tmA16 : p->sw_hp == 32 ? p->tmA32 : p->sw_hp == 64 ? p->tmA64 : p->tmA128;
       // 4 x 48 KB measured 2.26 ms against 2.30 ms for 5 x 40 KB on config 5 (3 runs each): the
       // ring is not the limit, so the 4-stage layout is the default (RB_SWEEP_BIG=0: the 5-stage one)

@@ -167,6 +167,8 @@ __device__ __forceinline__ void skinny_finish(const SkinnyArgs& a, const SkinnyI
     if (r < h) {
       const int64_t crow = a.row_perm ? (int64_t)a.row_perm[p0 + r] : (int64_t)p0 + r;  // CSR: identity
       store_c<VEC, ALIGNED>(a.C + crow * a.ldc + n, n, a.N, acc[r], a.accumulate != 0);
+      for (int f = 0; f < a.fan.n; ++f)  // fused all-gather: the same row into every peer's C
+        store_c<VEC, ALIGNED>(a.fan.p[f] + crow * a.ldc + n, n, a.N, acc[r], a.accumulate != 0);
     }
 }
 

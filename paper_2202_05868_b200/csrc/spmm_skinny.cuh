@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "common.cuh"
+
 #include <cuda_runtime.h>
 
 namespace rb {
@@ -36,6 +38,7 @@ struct SkinnyArgs {
   float* ws;      // split-row partials
   int32_t* cnt;   // split-row arrival counters (zero between launches)
   int32_t accumulate;  // 1: C += result (2:4 residual pass), 0: C = result
+  CFan fan;            // further copies of every C store (fused all-gather); fan.n = 0: none
 };
 
 // CSR operand of the comparator kernel (spmm_csr): the reference's CsrMatrix arrays on the device.

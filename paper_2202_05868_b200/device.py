@@ -406,6 +406,47 @@ class DeviceVbr:
         L.check(run(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0), L.stream_handle(stream)))
         return out
 
+    def spmm_fanout(self, B: torch.Tensor, out: torch.Tensor, peers=(), c_rows: torch.Tensor | None = None,
+                    precision: str | None = None, shard: int = 0, n_shards: int = 1, stream=None,
+                    validate: bool = True) -> torch.Tensor:
+        """Fused all-gather (rb_spmm_execute_fanout): C = A @ B into ``out`` (float32) and, by the
+        same epilogue stores, into every tensor of ``peers`` (the other ranks' full-size C mapped over
+        NVLink — dist.FusedGather — or any device buffers shaped like ``out``).  ``c_rows``: int32
+        device [n_rows], the output row of each permuted row (None: row_perm, out is [n_rows, N]);
+        a rank's sub-VBR passes its shard's global source rows (dist.shard_vbr sets
+        ``global_rows``), so ``out`` / ``peers`` are the full [n_rows_global, N] C."""
+        if B.dim() != 2 or B.shape[0] != self.n_cols:
+            raise ValueError(f"dimension mismatch: {self.n_cols} vs {B.shape[0] if B.dim() == 2 else B.shape}")
+        prec = precision or {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}[B.dtype]
+        if prec == "fp64":
+            raise ValueError("fan-out writes float32 C (no fp64 path)")
+        if L.TORCH_DTYPE[L.PRECISION[prec]] != B.dtype or B.stride(1) != 1:
+            raise ValueError("B must be row-major with the precision's dtype")
+        N = B.shape[1]
+        peers = list(peers)
+        if len(peers) > 7:
+            raise ValueError("at most 7 peers (8 ranks)")
+        for t in [out] + peers:
+            if (t.dtype != torch.float32 or t.dim() != 2 or t.shape != out.shape or t.stride() != out.stride()
+                    or t.stride(1) != 1 or out.shape[1] != N):
+                raise ValueError("out / peers must be float32 [rows, N] row-major buffers of one layout")
+        if c_rows is None:
+            if out.shape[0] != self.n_rows:
+                raise ValueError("out must have n_rows rows when c_rows is None")
+        else:
+            if c_rows.dtype != torch.int32 or c_rows.numel() != self.n_rows or not c_rows.is_contiguous():
+                raise ValueError("c_rows must be a contiguous int32 tensor of n_rows entries")
+            if validate and self.n_rows and not (0 <= int(c_rows.min()) and int(c_rows.max()) < out.shape[0]):
+                raise ValueError("c_rows out of range of out")
+        if N == 0 or self.n_rows == 0:
+            return out
+        h = self.plan(N, prec, shard, n_shards, stream)
+        arr = (ctypes.c_void_p * max(1, len(peers)))(*[L.ptr(t) for t in peers])
+        L.check(L.lib().rb_spmm_execute_fanout(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0), arr, len(peers),
+                                               L.ptr(c_rows) if c_rows is not None else None,
+                                               L.stream_handle(stream)))
+        return out
+
     # ---------------------------------------------------------------- reference-format views
     def host_structure(self):
         rp = self.row_partition.cpu().numpy().astype(np.int64)

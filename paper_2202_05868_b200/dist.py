@@ -3,9 +3,15 @@
 Each rank owns a contiguous, work-balanced range of PERMUTED rows (whole
 block-row M-tiles, ``rb_spmm_shard_range``), so it writes a disjoint set of C
 rows with no data-path collective.  B is replicated.  The only collective is the
-optional all-gather of C: every rank's rows (in permuted order) are gathered
-with ``torch.distributed.all_gather`` (NCCL over NVLink on the GPU
-box, gloo in the CPU tests) and un-permuted in place.
+optional all-gather of C, in two forms:
+
+* ``gather_c``: every rank's rows (in permuted order) are gathered with
+  ``torch.distributed.all_gather`` (NCCL over NVLink on the GPU box, gloo in the CPU tests) and
+  un-permuted in place — the baseline;
+* ``FusedGather``: the SpMM epilogues store every C element of the rank's rows, already at its
+  source row, into every rank's full-size C over NVLink (``rb_spmm_execute_fanout`` with the peers'
+  symmetric-memory buffers), so the gather overlaps the math and there is no collective call and no
+  un-permute pass; one device-side barrier orders the peers' writes before anyone reads.
 """
 
 from __future__ import annotations
@@ -112,9 +118,53 @@ def shard_vbr(dA, partition, row_perm, row_partition, precision: str, shard: int
     dv = DeviceVbr.build(sub, partition, torch.arange(e - b, dtype=torch.int64, device=rows.device), cuts,
                          dtypes=(precision,))
     dv.work_shards = n_shards  # plans size hub-row parts for a 1/n_shards share of the product
+    dv.global_rows = rows.to(torch.int32).contiguous()  # output rows for the fused gather (c_rows)
     return dv, (b, e), ranges
 
 
 def local_rows(C_full_layout: torch.Tensor, row_perm: torch.Tensor, begin: int, end: int) -> torch.Tensor:
     """This rank's rows (permuted order) out of a full-size C that the kernel wrote in source order."""
     return C_full_layout.index_select(0, row_perm[begin:end].to(C_full_layout.device))
+
+
+def global_rows_of(row_perm, begin: int, end: int) -> torch.Tensor:
+    """int32 output rows (source row ids) of permuted positions [begin, end): the c_rows a shard's
+    sub-VBR passes to the fused gather (C[row_perm[p]] = row p of the permuted product, multiply.py:90)."""
+    perm = row_perm if isinstance(row_perm, torch.Tensor) else torch.as_tensor(np.asarray(row_perm))
+    return perm[begin:end].to(torch.int32).contiguous()
+
+
+class FusedGather:
+    """Full-size float32 C [n_rows, N] on every rank in symmetric memory, plus views of every peer's
+    copy mapped into this process over NVLink (torch symmetric memory: P2P-mapped allocations).
+
+    ``run(dv, B)`` multiplies this rank's sub-VBR with rb_spmm_execute_fanout: the epilogues write the
+    rank's rows into its own buffer and all peers' buffers, then a device-side barrier (on the same
+    stream) makes every rank's rows visible to every rank.  Afterwards ``self.C`` holds the whole
+    product in source row order on every rank — what gather_c returns — with no NCCL call.
+    Needs a CUDA process group whose GPUs are NVLink peers."""
+
+    def __init__(self, n_rows: int, N: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.group = group or dist.group.WORLD
+        self.rank, self.world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        if self.world > 8:
+            raise ValueError("fused gather supports up to 8 ranks (7 peers)")
+        name = self.group.group_name
+        try:  # required by older torch releases, a no-op / absent in newer ones
+            symm_mem.enable_symm_mem_for_group(name)
+        except Exception:  # noqa: BLE001
+            pass
+        self.C = symm_mem.empty((n_rows, N), dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self.C, name)
+        self.peers = [self.handle.get_buffer(r, (n_rows, N), torch.float32) for r in range(self.world)
+                      if r != self.rank]
+
+    def run(self, dv, B: torch.Tensor, precision: str | None = None, stream=None) -> torch.Tensor:
+        rows = getattr(dv, "global_rows", None)
+        dv.spmm_fanout(B, self.C, self.peers, c_rows=rows, precision=precision, stream=stream, validate=False)
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.handle.barrier(channel=0)
+        return self.C

@@ -118,8 +118,15 @@ def _worker_subvbr(rank, world, port, name, q):
         pay = oracle.vbr_payloads(srp, sci, sval, case["boundaries"], ident, cuts, sbp, sbc)
         C_local = oracle.spmm_vbr_np(pay, ident, cuts, case["boundaries"], B)  # permuted order = local order
         full = rbdist.gather_c(torch.from_numpy(C_local), torch.from_numpy(case["row_perm"]), ranges)
+        # the fused gather's row map: the rank stores its rows at global_rows_of (= dv.global_rows,
+        # rb_spmm_execute_fanout's c_rows) in every rank's full C; disjoint rows, so summing the
+        # ranks' stores must give exactly the NCCL gather + un-permute result
+        fan = torch.zeros_like(full)
+        fan[rbdist.global_rows_of(case["row_perm"], b, e).to(torch.int64)] = torch.from_numpy(C_local)
+        dist.all_reduce(fan)
         if rank == 0:
             q.put(full.numpy())
+            q.put(fan.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -137,6 +144,7 @@ def test_sharded_sub_vbr_gather_matches_single_process(name, world):
     for p in procs:
         p.start()
     full = q.get(timeout=300)
+    fan = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -144,3 +152,4 @@ def test_sharded_sub_vbr_gather_matches_single_process(name, world):
                               case["row_partition"], case["blk_ptr"], case["blk_col"])
     ref = oracle.spmm_vbr_np(pay, case["row_perm"], case["row_partition"], case["boundaries"], B)
     np.testing.assert_allclose(full, ref, rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(fan, full)  # fused-gather row map == gather_c + un-permute
