@@ -372,6 +372,17 @@ def run_ours(args, world, rank):
                 "algorithmic_bytes_per_step": alg_bytes,
                 "executed_tflops": round(exec_tflops, 3),
                 "useful_tflops": round(achieved_tflops, 4)}
+        # The kernels these configs spend their time in gather one B row (N x elem bytes) per
+        # nonzero, mostly from L2. That stream, not HBM, is what they saturate first. The
+        # denominator is the L2-hit ld.global bandwidth that tools/l2bw measured on B200
+        # (profiles/r02/l2bw.txt: 10.0-10.4 TB/s at 16-128 MB working sets, 4 CTAs/SM).
+        gathered = dv.csr.nnz * N * esz
+        roof["l2_gather"] = {"bytes_per_step": gathered,
+                             "achieved_gbs": round(gathered / (ms_local * 1e-3) / 1e9, 1),
+                             "peak_gbs": L2_LDG_GBS,
+                             "frac": round(gathered / (ms_local * 1e-3) / 1e9 / L2_LDG_GBS, 4),
+                             "what": "nnz x N x elem bytes of gathered B rows per step (one B row per "
+                                     "nonzero) over the measured L2-hit ld.global bandwidth"}
     if roof["traffic"] and world == 1 and args.scale == 1:
         # the ncu DRAM bytes of one step over this run's step time: how close the step is to HBM
         roof["traffic_gbs"] = round(roof["traffic"] / (ms_local * 1e-3) / 1e9, 1)
@@ -396,6 +407,9 @@ def run_ours(args, world, rank):
             out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+L2_LDG_GBS = 10000.0  # L2-hit ld.global read bandwidth, tools/l2bw on B200 (profiles/r02/l2bw.txt)
 
 
 def run_gather(args, dv, B, C, prec, shard, world, flush, useful):
