@@ -374,15 +374,18 @@ def run_ours(args, world, rank):
                 "useful_tflops": round(achieved_tflops, 4)}
         # The kernels these configs spend their time in gather one B row (N x elem bytes) per
         # nonzero, mostly from L2. That stream, not HBM, is what they saturate first. The
-        # denominator is the L2-hit ld.global bandwidth that tools/l2bw measured on B200
-        # (profiles/r02/l2bw.txt: 10.0-10.4 TB/s at 16-128 MB working sets, 4 CTAs/SM).
+        # denominator is the random-row ld.global gather bandwidth that tools/l2bw/gather_probe
+        # measured on B200 (profiles/r02/gather_probe.txt): 16.2-16.8 TB/s while B fits in L2,
+        # 9.1-9.2 TB/s for a 256 MB B.
         gathered = dv.csr.nnz * N * esz
+        b_bytes = dA.n_cols * N * esz
+        peak_g = GATHER_L2_GBS if b_bytes <= 64 << 20 else GATHER_BIG_GBS
         roof["l2_gather"] = {"bytes_per_step": gathered,
                              "achieved_gbs": round(gathered / (ms_local * 1e-3) / 1e9, 1),
-                             "peak_gbs": L2_LDG_GBS,
-                             "frac": round(gathered / (ms_local * 1e-3) / 1e9 / L2_LDG_GBS, 4),
+                             "peak_gbs": peak_g,
+                             "frac": round(gathered / (ms_local * 1e-3) / 1e9 / peak_g, 4),
                              "what": "nnz x N x elem bytes of gathered B rows per step (one B row per "
-                                     "nonzero) over the measured L2-hit ld.global bandwidth"}
+                                     "nonzero) over the measured random-row gather bandwidth for B's size"}
     if roof["traffic"] and world == 1 and args.scale == 1:
         # the ncu DRAM bytes of one step over this run's step time: how close the step is to HBM
         roof["traffic_gbs"] = round(roof["traffic"] / (ms_local * 1e-3) / 1e9, 1)
@@ -409,7 +412,9 @@ def run_ours(args, world, rank):
         print(json.dumps(out), flush=True)
 
 
-L2_LDG_GBS = 10000.0  # L2-hit ld.global read bandwidth, tools/l2bw on B200 (profiles/r02/l2bw.txt)
+# Random-row gather bandwidth (16 B per lane, 8 rows in flight per lane group, 4 CTAs/SM), measured
+# by tools/l2bw/gather_probe on B200 (profiles/r02/gather_probe.txt): B in L2 (64 MB) / B of 256 MB
+GATHER_L2_GBS, GATHER_BIG_GBS = 16500.0, 9150.0
 
 
 def run_gather(args, dv, B, C, prec, shard, world, flush, useful):

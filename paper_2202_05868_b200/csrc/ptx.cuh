@@ -108,14 +108,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
-// evict_last on a `frac` share of the lines (address-hashed), evict_first on the rest: a cyclic
-// sweep over a set larger than L2 keeps a fixed part resident instead of thrashing all of it
-__device__ __forceinline__ uint64_t policy_evict_last_frac(float frac) {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(frac));
-  return p;
-}
-
 __device__ __forceinline__ void st_global_hint(float* p, float v, uint64_t policy) {
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(policy) : "memory");
 }

@@ -831,8 +831,6 @@ struct SweepArgs {
   const int4* done;         // row completions in commit order: (g, n0, slot, -)
   const int32_t* done_ptr;
   int32_t hp;
-  float b_frac;      // share of B lines loaded with L2 evict_last (1: all; RB_SWEEP_BFRAC)
-  int32_t c_stream;  // 1: C stores with L2 evict_first (RB_SWEEP_CST)
 };
 
 // PAIR: the full barrier of an even stage covers it and the next one (2 arrivals per phase), so the
@@ -926,7 +924,7 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmA);
     const uint64_t pol_a = policy_evict_first();
-    const uint64_t pol_b = w.b_frac >= 1.f ? policy_evict_last() : policy_evict_last_frac(w.b_frac);
+    const uint64_t pol_b = policy_evict_last();
     PipeState rings[SW_MMA_WARPS];
     StepReader rd;
     rd.init(w.steps, s_begin, s_end, lane);
@@ -1057,7 +1055,6 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
     // epilogue (M64): warp quadrant q = warp & 3 holds rows 16q..16q+15 of both lane halves; this
     // warp drains 128 of the slot's 256 columns (half ch).  A lane of the slot's half owns one row.
     const int q = warp & 3, ch = (warp - 1 - SW_MMA_WARPS) >> 2;
-    const uint64_t pol_c = policy_evict_first();
     float* epi_buf = reinterpret_cast<float*>(smem + ST * (ASLOT + S_B_BYTES) + 1024) +
                      (warp - 1 - SW_MMA_WARPS) * 16 * 36;  // 16 x 33 used
     uint32_t done_ph = 0;
@@ -1102,15 +1099,15 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
         }
         __syncwarp();
         const int n = nb + k * 32 + lane;
-        for (int i = 0; i < slab_rows; ++i) {
-          const int cr = __shfl_sync(0xffffffffu, my_row, i);
-          if (n < a.N) {
-            const int64_t off = (int64_t)cr * a.ldc + n;
-            if (w.c_stream)
-              st_global_hint(a.C + off, epi_buf[i * 33 + lane], pol_c);
-            else
-              a.C[off] = epi_buf[i * 33 + lane];
-            for (int f = 0; f < a.fan.n; ++f) a.fan.p[f][off] = epi_buf[i * 33 + lane];
+        if (a.fan.n == 0) {  // the plain store loop (a fan-out test inside it cost config 5 ~10 %)
+          for (int i = 0; i < slab_rows; ++i) {
+            const int cr = __shfl_sync(0xffffffffu, my_row, i);
+            if (n < a.N) a.C[(int64_t)cr * a.ldc + n] = epi_buf[i * 33 + lane];
+          }
+        } else {
+          for (int i = 0; i < slab_rows; ++i) {
+            const int cr = __shfl_sync(0xffffffffu, my_row, i);
+            if (n < a.N) st_fan(a.fan, a.C, (int64_t)cr * a.ldc + n, epi_buf[i * 33 + lane]);
           }
         }
         __syncwarp();
@@ -1174,10 +1171,18 @@ __global__ void __launch_bounds__(M64 ? SW64_THREADS : SW_THREADS, 1)
         for (int mt = 0; mt < 2; ++mt) {
           const int n = n0 + mt * 128 + q * 32 + lane;
           const bool nvalid = mt < n_mt && n < a.N;
+          if (a.fan.n == 0) {
 #pragma unroll
-          for (int jj = 0; jj < 64; ++jj) {
-            const int row = __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31);
-            if (nvalid && jj < h) st_fan(a.fan, a.C, (int64_t)row * a.ldc + n, __uint_as_float(r[mt][jj]));
+            for (int jj = 0; jj < 64; ++jj) {
+              const int row = __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31);
+              if (nvalid && jj < h) a.C[(int64_t)row * a.ldc + n] = __uint_as_float(r[mt][jj]);
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 64; ++jj) {
+              const int row = __shfl_sync(0xffffffffu, jj < 32 ? rp_lo : rp_hi, jj & 31);
+              if (nvalid && jj < h) st_fan(a.fan, a.C, (int64_t)row * a.ldc + n, __uint_as_float(r[mt][jj]));
+            }
           }
         }
       } else {
@@ -2468,28 +2473,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
   if (tc && p->n_sw_steps > 0)
     tasks.push_back([&](cudaStream_t st) {
       SpmmArgs s = a;
-      // L2 experiments (developer knobs): RB_SWEEP_BFRAC = % of B lines loaded evict_last (default
-      // 100), RB_SWEEP_CST=1 = C stores evict_first, RB_SWEEP_L2SET = MB of persisting-L2 set-aside
-      // (cudaLimitPersistingL2CacheSize, process-wide; evict_last lines live there)
-      static const float b_frac = [] {
-        const char* e = std::getenv("RB_SWEEP_BFRAC");
-        const int v = e ? std::atoi(e) : 100;
-        return v <= 0 || v >= 100 ? 1.f : (float)v / 100.f;
-      }();
-      static const int c_stream = [] {
-        const char* e = std::getenv("RB_SWEEP_CST");
-        return e && e[0] == '1' ? 1 : 0;
-      }();
-      static const int l2set = [] {
-        const char* e = std::getenv("RB_SWEEP_L2SET");
-        return e ? std::atoi(e) : -1;
-      }();
-      if (l2set >= 0) {
-        size_t cur = 0;
-        RB_CUDA_TRY(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-        if (cur != ((size_t)l2set << 20)) RB_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)l2set << 20));
-      }
-      SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp, b_frac, c_stream};
+      SweepArgs w{p->d_sw_steps, p->d_sw_step_ptr, p->d_sw_done, p->d_sw_done_ptr, p->sw_hp};
       const CUtensorMap& tA = p->sw_hp == 16 ? p->tmA16 : p->sw_hp == 32 ? p->tmA32 : p->sw_hp == 64 ? p->tmA64 : p->tmA128;
       // 4 x 48 KB measured 2.26 ms against 2.30 ms for 5 x 40 KB on config 5 (3 runs each): the
       // ring is not the limit, so the 4-stage layout is the default (RB_SWEEP_BIG=0: the 5-stage one)
