@@ -17,8 +17,6 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
-#include <cstdlib>
-
 #include "common.cuh"
 #include "spmm_skinny.cuh"
 
@@ -587,116 +585,6 @@ __device__ __forceinline__ void csr_item(const SkinnyArgs& a, const CsrArgs& c, 
   skinny_finish<1, VEC, LPR, ALIGNED>(a, it, cols, 1, it.g, n, gl, gmask, acc);
 }
 
-// Cross-item prefetch form of csr_item.  A config-3 row has ~16 nonzeros, so an item is only one or
-// two gather batches long, and the per-item chain (claim -> item -> row_ptr -> col/val -> B rows ->
-// FMA -> store) left each dependent latency exposed once per item.  Here the group claims the next
-// item at the start of the current one, issues the next item's descriptor / row_ptr / first
-// (col, val) loads right behind the current item's first B gathers, and loads each chunk's
-// (col, val) one chunk ahead, so only the B gathers and the store stay on the critical path.
-#ifndef RB_CSR_PF_MIN_BLOCKS
-#define RB_CSR_PF_MIN_BLOCKS 4
-#endif
-struct CsrHead {
-  int32_t g, n0, part, nparts, slot, wsoff;
-  int64_t j0, j1;
-  int col;
-  float val;
-};
-
-template <typename T>
-__device__ __forceinline__ void csr_colval(const CsrArgs& c, int64_t j, bool pred, int& col, float& val) {
-  col = 0;
-  val = 0.f;
-  if (pred) {
-    if (c.col32) {
-      col = __ldg(c.col32 + j);
-      val = __ldg(c.val32 + j);
-    } else {
-      col = (int)__ldg(c.col_idx + j);
-      val = round_to<T>(__ldg(c.values + j));
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void csr_head(const SkinnyArgs& a, const CsrArgs& c, int64_t i, int gl, CsrHead& h) {
-  h.j0 = h.j1 = 0;
-  if (i >= a.n_items) return;
-  const SkinnyItem it = load_item(a.items + i);
-  h.g = it.g;
-  h.n0 = it.n0;
-  h.part = it.part;
-  h.nparts = it.nparts;
-  h.slot = it.slot;
-  h.wsoff = it.wsoff;
-  const int64_t base = c.row_ptr[it.g];
-  h.j0 = base + it.bb;
-  h.j1 = base + it.be;
-  csr_colval<T>(c, h.j0 + gl, gl < h.j1 - h.j0, h.col, h.val);
-}
-
-template <typename T, int LPR, bool ALIGNED>
-__device__ __forceinline__ void csr_item_pf(const SkinnyArgs& a, const CsrArgs& c, CsrHead& h, int64_t inext, int cols,
-                                            int gl, unsigned gmask) {
-  constexpr int VEC = 16 / sizeof(T);
-  const int n = h.n0 + gl * VEC;
-  const T* Bn = static_cast<const T*>(a.B) + n;
-  const int64_t ldb = a.ldb;
-  float acc[1][VEC];
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) acc[0][e] = 0.f;
-  CsrHead nx;
-  bool issued = false;
-  int col = h.col;
-  float val = h.val;
-  for (int64_t j0 = h.j0; j0 < h.j1; j0 += LPR) {
-    const int cnt = (int)(h.j1 - j0 < LPR ? h.j1 - j0 : LPR);
-    int ncol;
-    float nval;
-    csr_colval<T>(c, j0 + LPR + gl, j0 + LPR + gl < h.j1, ncol, nval);  // next chunk, one ahead
-    for (int i = 0; i < cnt; i += 8) {
-      float av[8];
-      uint4 bv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = __shfl_sync(gmask, col, (i + u) & (LPR - 1), LPR);
-        av[u] = __shfl_sync(gmask, val, (i + u) & (LPR - 1), LPR);
-        if (i + u < cnt) bv[u] = load_b_raw<T, ALIGNED>(Bn + (int64_t)k * ldb, n, a.N);
-      }
-      if (!issued) {  // the next item's loads go out behind this item's first gathers
-        csr_head<T>(a, c, inext, gl, nx);
-        issued = true;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (i + u < cnt) fma_row<T>(acc[0], av[u], bv[u]);
-    }
-    col = ncol;
-    val = nval;
-  }
-  if (!issued) csr_head<T>(a, c, inext, gl, nx);
-  const SkinnyItem it{h.g, h.n0, 0, 0, h.part, h.nparts, h.slot, h.wsoff};
-  skinny_finish<1, VEC, LPR, ALIGNED>(a, it, cols, 1, h.g, n, gl, gmask, acc);
-  h = nx;
-}
-
-template <typename T, int LPR, bool ALIGNED>
-__global__ void __launch_bounds__(256, RB_CSR_PF_MIN_BLOCKS) spmm_csr_pf_kernel(SkinnyArgs a, CsrArgs c, int cols,
-                                                                             unsigned long long* sched) {
-  constexpr int GPW = 32 / LPR;
-  const int lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
-  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
-  int64_t i = next_item<LPR>(sched, gl, gmask);
-  CsrHead h;
-  csr_head<T>(a, c, i, gl, h);
-  while (i < a.n_items) {
-    const int64_t inext = next_item<LPR>(sched, gl, gmask);
-    csr_item_pf<T, LPR, ALIGNED>(a, c, h, inext, cols, gl, gmask);
-    i = inext;
-  }
-  leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
-}
-
 template <typename T, int LPR, bool ALIGNED>
 // 4 resident CTAs per SM (<= 64 registers, a few spills): twice the gathers in flight of the
 // 2-CTA build; config 3 1.08 -> 0.86 ms, 2b 7.50 -> 6.50 ms, config 1 +6 % (latency-bound, tiny).
@@ -765,12 +653,7 @@ int launch_csr_t(const SkinnyArgs& a, const CsrArgs& c, int cols, unsigned long 
   const bool aligned = ((a.ldb * (int64_t)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0) &&
                        (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
   unsigned grid = 0;
-  static const bool pf = [] {  // RB_CSR_PF=0: the per-item form
-    const char* e = std::getenv("RB_CSR_PF");
-    return !(e && e[0] == '0');
-  }();
-  auto k = pf ? (aligned ? spmm_csr_pf_kernel<T, LPR, true> : spmm_csr_pf_kernel<T, LPR, false>)
-              : (aligned ? spmm_csr_kernel<T, LPR, true> : spmm_csr_kernel<T, LPR, false>);
+  auto k = aligned ? spmm_csr_kernel<T, LPR, true> : spmm_csr_kernel<T, LPR, false>;
   int rc = persistent_grid(k, 0, a.n_items, 8 * (32 / LPR), &grid);
   if (rc) return rc;
   k<<<grid, 256, 0, stream>>>(a, c, cols, sched);
