@@ -114,3 +114,37 @@ def test_fanout_argument_checks():
     rc = L.lib().rb_spmm_execute_fanout(h, L.ptr(B), B.stride(0), L.ptr(out), out.stride(0), many, 8, None,
                                         L.stream_handle())
     assert rc != 0
+
+
+@pytest.mark.timeout(300)
+def test_fused_gather_symmetric_memory_world1():
+    """dist.FusedGather's plumbing on a real device: NCCL process group, torch symmetric-memory C,
+    rendezvous and the device barrier, at world size 1 (no peers; one GPU is all this pod has).
+    The gathered C must equal the plain product bit for bit."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2202_05868_b200 import dist as rbdist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        A, q, V, Bh = _vbr("cfg5_s32")
+        B = torch.from_numpy(Bh).to(torch.bfloat16).cuda()
+        plain = V.device.spmm(B, precision="bf16")
+        try:
+            fg = rbdist.FusedGather(A.n_rows, B.shape[1], torch.device("cuda:0"))
+        except Exception as exc:  # noqa: BLE001
+            pytest.skip(f"torch symmetric memory unavailable here: {type(exc).__name__}: {exc}")
+        assert fg.peers == []
+        C = fg.run(V.device, B, precision="bf16")
+        torch.cuda.synchronize()
+        assert torch.equal(C, plain)
+    finally:
+        dist.destroy_process_group()
