@@ -1283,24 +1283,33 @@ __global__ void __launch_bounds__(SIMT_COLS) spmm_simt_kernel(SpmmArgs a, const 
 }
 
 // ------------------------------------------------------------------------------------------
-// Rows of block rows without stored blocks: C[row_perm[pos], 0:N] = 0, one warp per row, float4
-// stores (multiply.py:85-86 leaves them exactly 0).
+// Rows of block rows without stored blocks: C[row_perm[pos], 0:N] = 0 with float4 stores
+// (multiply.py:85-86 leaves them exactly 0).  A warp takes 32 rows at a time: each lane resolves
+// one row's offset (one coalesced pos[] load and one row_perm gather for all 32), then the warp
+// zeroes the rows one after another.  One dependent-load chain per 32 rows instead of per row keeps
+// the kernel store-bound.
 __global__ void __launch_bounds__(256) zero_rows_kernel(const int32_t* __restrict__ pos, int64_t n,
                                                         const int32_t* __restrict__ row_perm, float* C, int64_t ldc,
                                                         int32_t N, CFan fan) {
   const int lane = threadIdx.x & 31;
   const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t off = (int64_t)row_perm[pos[w]] * ldc;
-    for (int f = -1; f < fan.n; ++f) {  // C, then every fan-out copy
-      float* dst = (f < 0 ? C : fan.p[f]) + off;
-      if (vec) {
-        const int n4 = N >> 2;
-        for (int c = lane; c < n4; c += 32) reinterpret_cast<float4*>(dst)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int c = (n4 << 2) + lane; c < N; c += 32) dst[c] = 0.f;
-      } else {
-        for (int c = lane; c < N; c += 32) dst[c] = 0.f;
+  const int n4 = N >> 2;
+  const int64_t n_batches = (n + 31) >> 5;
+  for (int64_t bt = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; bt < n_batches;
+       bt += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r0 = bt << 5;
+    const int cnt = n - r0 < 32 ? (int)(n - r0) : 32;
+    const int64_t my_off = lane < cnt ? (int64_t)row_perm[pos[r0 + lane]] * ldc : 0;
+    for (int j = 0; j < cnt; ++j) {
+      const int64_t off = __shfl_sync(0xffffffffu, my_off, j);
+      for (int f = -1; f < fan.n; ++f) {  // C, then every fan-out copy
+        float* dst = (f < 0 ? C : fan.p[f]) + off;
+        if (vec) {
+          for (int c = lane; c < n4; c += 32) reinterpret_cast<float4*>(dst)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c = (n4 << 2) + lane; c < N; c += 32) dst[c] = 0.f;
+        } else {
+          for (int c = lane; c < N; c += 32) dst[c] = 0.f;
+        }
       }
     }
   }
@@ -2341,7 +2350,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
   std::vector<std::function<int(cudaStream_t)>> tasks;
   if (p->n_zero > 0)
     tasks.push_back([&](cudaStream_t st) {
-      const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 7) / 8, 148 * 16);
+      const unsigned grid = (unsigned)std::min<int64_t>((p->n_zero + 255) / 256, 148 * 16);  // 8 warps x 32 rows
       // fp64 C: a row of N doubles is 2N zero floats
       const int w = p->b_dtype == RB_F64 ? 2 : 1;
       zero_rows_kernel<<<grid, 256, 0, st>>>(p->d_zero, p->n_zero, out_rows, C, ldc * w, (int32_t)p->N * w, fan);
