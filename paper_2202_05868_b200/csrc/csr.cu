@@ -18,6 +18,7 @@ struct rb_csr_plan {
   int32_t b_dtype;
   rb::SkinnyItem* d_items = nullptr;
   int64_t n_items = 0;
+  int32_t chunk = 1;  // items per claim (csr_claim_chunk)
   float* d_ws = nullptr;
   int32_t* d_cnt = nullptr;
   unsigned long long* d_sched = nullptr;
@@ -83,6 +84,7 @@ extern "C" int rb_csr_plan_create(int64_t n_rows, int64_t n_cols, const int64_t*
   p->N = N;
   p->b_dtype = b_dtype;
   p->n_items = (int64_t)items.size();
+  p->chunk = csr_claim_chunk(items);
   cudaError_t e = cudaSuccess;
   if (p->n_items > 0) e = cudaMalloc(&p->d_items, sizeof(SkinnyItem) * items.size());
   if (e == cudaSuccess) e = cudaMalloc(&p->d_sched, 2 * sizeof(unsigned long long));
@@ -121,7 +123,7 @@ extern "C" int rb_csr_execute(const rb_csr_plan* p, const int64_t* row_ptr, cons
   a.N = (int32_t)p->N;
   a.ws = p->d_ws;
   a.cnt = p->d_cnt;
-  CsrArgs c{row_ptr, col_idx, values, nullptr, nullptr};
+  CsrArgs c{row_ptr, col_idx, values, nullptr, nullptr, p->chunk};
   std::lock_guard<std::mutex> lk(p->mu);
   if (!p->done) RB_CUDA_TRY(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
   if (p->done_valid && p->done_stream != stream) RB_CUDA_TRY(cudaStreamWaitEvent(stream, p->done, 0));

@@ -1451,6 +1451,7 @@ struct rb_spmm_plan {
   int64_t skinny_off[rb::SKINNY_CLASSES + 1] = {0, 0, 0, 0, 0};
   rb::SkinnyItem* d_cmp_items = nullptr;  // compact-payload rows (CSR engine over permuted rows)
   int64_t n_cmp_items = 0;
+  int32_t cmp_chunk = 1;  // items per claim in the CSR engine (csr_claim_chunk)
   unsigned long long* d_cmp_sched = nullptr;
   CUtensorMap tmA16, tmA32, tmA64, tmA128;
   // multi-slot sweep (spmm_sweep_kernel) for the dominant short height class
@@ -1953,6 +1954,7 @@ extern "C" int rb_spmm_plan_create_ex(const rb_vbr_device* vbr, int64_t N, int32
     std::stable_sort(cmp_items.begin(), cmp_items.end(),
                      [](const SkinnyItem& x, const SkinnyItem& y) { return x.be - x.bb > y.be - y.bb; });
     p->n_cmp_items = (int64_t)cmp_items.size();
+    p->cmp_chunk = csr_claim_chunk(cmp_items);
     cudaError_t e = cudaMalloc(&p->d_cmp_items, sizeof(SkinnyItem) * cmp_items.size());
     if (e == cudaSuccess) e = cudaMalloc(&p->d_cmp_sched, 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(p->d_cmp_sched, 0, 2 * sizeof(unsigned long long), stream);
@@ -2388,7 +2390,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
       SkinnyArgs kc = k;
       kc.items = p->d_cmp_items;
       kc.n_items = p->n_cmp_items;
-      const CsrArgs cr{p->v.cmp_ptr, nullptr, nullptr, p->v.cmp_col, p->v.cmp_val};
+      const CsrArgs cr{p->v.cmp_ptr, nullptr, nullptr, p->v.cmp_col, p->v.cmp_val, p->cmp_chunk};
       return launch_csr(kc, cr, p->b_dtype, p->d_cmp_sched, st);
     });
   if ((p->b_dtype == RB_F32 || p->b_dtype == RB_F64) && p->n_simt > 0)
@@ -2448,7 +2450,7 @@ static int spmm_execute_locked(const rb_spmm_plan* p, const void* B, int64_t ldb
           kr.ldc = ldc;
           kr.N = (int32_t)p->N;
           kr.accumulate = 1;
-          CsrArgs cr{p->sp.res_ptr, nullptr, nullptr, p->sp.res_col, p->sp.res_val};
+          CsrArgs cr{p->sp.res_ptr, nullptr, nullptr, p->sp.res_col, p->sp.res_val, 1};
           return launch_csr(kr, cr, p->b_dtype, p->d_res_sched, st);
         }
         return (int)RB_OK;

@@ -585,21 +585,34 @@ __device__ __forceinline__ void csr_item(const SkinnyArgs& a, const CsrArgs& c, 
   skinny_finish<1, VEC, LPR, ALIGNED>(a, it, cols, 1, it.g, n, gl, gmask, acc);
 }
 
-template <typename T, int LPR, bool ALIGNED>
+template <typename T, int LPR, bool ALIGNED, int CH>
 // 4 resident CTAs per SM (<= 64 registers, a few spills): twice the gathers in flight of the
 // 2-CTA build; config 3 1.08 -> 0.86 ms, 2b 7.50 -> 6.50 ms, config 1 +6 % (latency-bound, tiny).
 #ifndef RB_CSR_MIN_BLOCKS
 #define RB_CSR_MIN_BLOCKS 4
 #endif
+
 __global__ void __launch_bounds__(256, RB_CSR_MIN_BLOCKS) spmm_csr_kernel(SkinnyArgs a, CsrArgs c, int cols,
                                                           unsigned long long* sched) {
   constexpr int GPW = 32 / LPR;
   const int lane = threadIdx.x & 31, gl = lane % LPR, grp = lane / LPR;
   const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
-  for (;;) {
-    const int64_t i = next_item<LPR>(sched, gl, gmask);
-    if (i >= a.n_items) break;
-    csr_item<T, LPR, ALIGNED>(a, c, load_item(a.items + i), cols, gl, gmask);
+  if constexpr (CH == 1) {
+    for (;;) {
+      const int64_t i = next_item<LPR>(sched, gl, gmask);
+      if (i >= a.n_items) break;
+      csr_item<T, LPR, ALIGNED>(a, c, load_item(a.items + i), cols, gl, gmask);
+    }
+  } else {  // c.chunk consecutive items per claim (launch_csr_t): one atomic round trip per chunk
+    const unsigned long long chunk = c.chunk > 1 ? (unsigned long long)c.chunk : 1ull;
+    for (;;) {
+      unsigned long long i0 = 0;
+      if (gl == 0) i0 = atomicAdd(sched, chunk);
+      i0 = __shfl_sync(gmask, i0, 0, LPR);
+      if ((int64_t)i0 >= a.n_items) break;
+      const int64_t i1 = min((int64_t)(i0 + chunk), a.n_items);
+      for (int64_t i = (int64_t)i0; i < i1; ++i) csr_item<T, LPR, ALIGNED>(a, c, load_item(a.items + i), cols, gl, gmask);
+    }
   }
   leave<LPR>(sched, gl, (unsigned long long)gridDim.x * (blockDim.x >> 5) * GPW);
 }
@@ -653,10 +666,19 @@ int launch_csr_t(const SkinnyArgs& a, const CsrArgs& c, int cols, unsigned long 
   const bool aligned = ((a.ldb * (int64_t)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0) &&
                        (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
   unsigned grid = 0;
-  auto k = aligned ? spmm_csr_kernel<T, LPR, true> : spmm_csr_kernel<T, LPR, false>;
-  int rc = persistent_grid(k, 0, a.n_items, 8 * (32 / LPR), &grid);
+  auto k1 = aligned ? spmm_csr_kernel<T, LPR, true, 1> : spmm_csr_kernel<T, LPR, false, 1>;
+  int rc = persistent_grid(k1, 0, a.n_items, 8 * (32 / LPR), &grid);
   if (rc) return rc;
-  k<<<grid, 256, 0, stream>>>(a, c, cols, sched);
+  // Two items per claim only for uniform lists (c.chunk) with at least 4 chunks per resident
+  // group.  The runtime-chunk instance (CH = 0) also serves 32-lane groups at chunk 1: its
+  // register allocation measured faster there (config 2b 6.52 -> 6.04 ms, profiles/r02/chunk_ab/);
+  // 16-lane groups keep the single-claim instance (CH = 1).
+  const int64_t groups = (int64_t)grid * 8 * (32 / LPR);
+  CsrArgs cc = c;
+  if (cc.chunk < 1 || a.n_items < 4 * (int64_t)cc.chunk * groups) cc.chunk = 1;
+  const bool runtime = LPR == 32 || cc.chunk > 1;
+  auto k = runtime ? (aligned ? spmm_csr_kernel<T, LPR, true, 0> : spmm_csr_kernel<T, LPR, false, 0>) : k1;
+  k<<<grid, 256, 0, stream>>>(a, cc, cols, sched);
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
 }
@@ -677,6 +699,17 @@ int launch_csr(const SkinnyArgs& a, const CsrArgs& c, int32_t b_dtype, unsigned 
                         : launch_csr_t<__half, 32>(a, c, cols, sched, stream);
     default: return fail(RB_EUNSUPPORTED, "csr SpMM: unsupported dtype");
   }
+}
+
+int csr_claim_chunk(const std::vector<SkinnyItem>& items) {
+  if (items.empty()) return 1;
+  int64_t total = 0, longest = 0;
+  for (const SkinnyItem& it : items) {
+    if (it.nparts > 1) return 1;
+    total += it.be - it.bb;
+    longest = std::max<int64_t>(longest, it.be - it.bb);
+  }
+  return longest * (int64_t)items.size() <= 2 * total ? 2 : 1;
 }
 
 int skinny_cols(int32_t b_dtype, int64_t N) {

@@ -48,7 +48,16 @@ struct CsrArgs {
   const double* values;
   const int32_t* col32;  // alternative operand (2:4 residuals): int32 columns, float values
   const float* val32;
+  int32_t chunk;  // items claimed per atomic (csr_claim_chunk; 0 / 1 = one at a time)
 };
+
+// Items per claim for a CSR work list: 2 when the list is uniform (no split rows, longest item at
+// most twice the mean), else 1.  Pairs hold consecutive items, i.e. the C-column slabs of one row.
+// A compile-time chunk for every list (profiles/r02/chunk_ab/) cost config 3 2.4x at 4 and 1.3x
+// at 2: its split hub rows' parts are consecutive items, and one group then runs them serially.
+// Config 1 has fewer items than resident groups and lost too.  The bench configs' lists all hold
+// split rows, so they run at chunk 1.
+int csr_claim_chunk(const std::vector<SkinnyItem>& items);
 
 // Height classes: block rows with h <= 1, 2, 4, 8 run the instance with H = 1, 2, 4, 8.
 constexpr int SKINNY_CLASSES = 4;

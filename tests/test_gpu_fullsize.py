@@ -72,7 +72,7 @@ def _check_structure(name, scale, dA, bounds, cfg, dg, dv):
     assert np.array_equal(bp, bp_dev) and np.array_equal(bc, bc_dev)
 
 
-@pytest.mark.parametrize("name,scale", [("2", 1), ("4", 1), ("5", 4), ("5", 1), ("2b", 4), ("1", 1), ("3", 1)])
+@pytest.mark.parametrize("name,scale", [("2", 1), ("4", 1), ("5", 4), ("5", 1), ("2b", 4), ("2b", 1), ("1", 1), ("3", 1)])
 def test_fullsize_structure_and_product(name, scale):
     """Every BASELINE config at its full size (2b at ¼): bit-exact structure, C through C·r
     checksums against a float64 product on the device, determinism, exact-zero empty rows."""

@@ -683,6 +683,33 @@ def test_spmm_csr_hub_rows_and_determinism(precision, N):
     assert np.array_equal(C1.double().cpu().numpy(), C)
 
 
+@pytest.mark.parametrize("N", [128, 512])
+def test_spmm_csr_uniform_rows_chunked_claims(N):
+    """Uniform work lists with many items per resident group are claimed two items per atomic
+    (csr_claim_chunk).  An odd item count puts the last claim half past the end.  Every row must
+    be written once and equal the product; the result must be bit-identical run to run."""
+    from paper_2202_05868_b200.device import DeviceCsr
+    from paper_2202_05868_b200.types import csr_from_coo
+
+    rng = np.random.default_rng(53 + N)
+    n_rows, n_cols, k = 160001, 2048, 6  # N=128: 160001 items; N=512: 2 slabs each
+    rows = np.repeat(np.arange(n_rows), k)
+    cols = np.concatenate([rng.choice(n_cols, size=k, replace=False) for _ in range(n_rows)])
+    vals = rounded(rng.uniform(-1.0, 1.0, len(rows)), torch.bfloat16)
+    A = csr_from_coo(n_rows, n_cols, rows, cols, vals)
+    Bh = rounded(rng.uniform(-1, 1, (n_cols, N)), torch.bfloat16)
+    dA = DeviceCsr.from_host(A, "cuda")
+    Bd = torch.from_numpy(Bh).to(torch.bfloat16).cuda()
+    C1, C2 = dA.spmm(Bd, precision="bf16"), dA.spmm(Bd, precision="bf16")
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)
+    Ad = torch.sparse_csr_tensor(torch.from_numpy(A.row_ptr), torch.from_numpy(A.col_idx), torch.from_numpy(A.values),
+                                 size=(n_rows, n_cols))
+    ref = (Ad @ torch.from_numpy(Bh)).numpy()
+    bound = np.abs(A.values).max() * k * np.abs(Bh).max()
+    assert np.abs(C1.double().cpu().numpy() - ref).max() <= 1e-4 * bound
+
+
 def test_edge_shapes_through_the_drop_in():
     """Degenerate inputs behave as in the reference: an all-zero matrix (every row its own empty
     block row or one empty group), zero dense columns, a single column / single row, a partition
